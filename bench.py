@@ -1,0 +1,291 @@
+#!/usr/bin/env python3
+"""Layout cost-evals/sec of the B200 hetsched fitness path (BASELINE.json metric).
+
+Workload (BASELINE config 2, the paper setting): N=64 devices, D_PP=8 x
+D_DP=8, GPT3-XL volumes (c_pp=1,073,741,824 B, c_dp=301,989,888 B), case-5
+world-wide matrix from the reference generator (seed 0).  A step is one
+pass of the fitness kernel over one population of P uniformly random
+balanced layouts per GPU.  Multi-GPU: the population is sharded (weak
+scaling, no data-path collective); time is the max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "layout cost-evals/sec (N=64, D_PP=8xD_DP=8)"
+WORKLOAD = ("paper setting: 64 devices, D_PP=8 x D_DP=8, GPT3-XL tasklets "
+            "(c_pp=1073741824 B, c_dp=301989888 B), case 5 world_geo matrix (seed 0)")
+# algorithmic on-chip work per evaluation at 8x8:
+# 2,240 fp64 table gathers (17,920 B) + Held-Karp 3,584 reads + 1,016 writes (36,800 B)
+SMEM_BYTES_PER_EVAL = 17_920 + 36_800
+HBM_BYTES_PER_EVAL = 64 * 2 + 3 * 8
+SMEM_BYTES_PER_CLK_SM = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--population", type=int, default=1 << 20, help="layouts per GPU per step")
+    ap.add_argument("--case", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def instance():
+    from paper_2206_01288_b200 import PAPER_WORKLOAD, scenario_case
+    return scenario_case(ARGS.case).graph(), PAPER_WORKLOAD
+
+
+def cpu_oracle_rate(g, w, seconds: float, threads: int):
+    """Oracle evals/s on a bounded sample (test infrastructure, CPU baseline only)."""
+    from oracle import oracle as O
+    orc = O.Oracle.of(g, w)
+    rng = np.random.default_rng(12345)
+    probe = np.sort(rng.permuted(np.tile(np.arange(64, dtype=np.int16), (400, 1)), axis=1).reshape(-1, 8, 8), axis=2)
+    t0 = time.perf_counter()
+    orc.comm_cost_batch(probe, threads=1)
+    per_core = len(probe) / (time.perf_counter() - t0)
+    count = int(max(threads * 200, per_core * threads * seconds))
+    parts = np.sort(rng.permuted(np.tile(np.arange(64, dtype=np.int16), (count, 1)), axis=1).reshape(-1, 8, 8),
+                    axis=2)
+    t0 = time.perf_counter()
+    orc.comm_cost_batch(parts, threads=threads)
+    dt = time.perf_counter() - t0
+    return count / dt, count, dt
+
+
+def run_reference():
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    g, w = instance()
+    threads = O.cpu_count()
+    rates = []
+    per_step = max(ARGS.cpu_seconds / max(ARGS.steps, 1), 1.0)
+    for i in range(ARGS.warmup + ARGS.steps):
+        r, count, dt = cpu_oracle_rate(g, w, per_step if i >= ARGS.warmup else 0.3, threads)
+        if i >= ARGS.warmup:
+            rates.append((count, dt))
+    total = sum(c for c, _ in rates)
+    secs = sum(d for _, d in rates)
+    value = total / secs
+    sample = f"{total} random 8x8 case-{ARGS.case} layouts over {ARGS.steps} steps, C oracle port of comm_cost"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "steps": ARGS.steps, "warmup": ARGS.warmup, "ms_per_step": 1000 * secs / ARGS.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic random balanced layouts", "config": {"workload": WORKLOAD},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours():
+    import torch
+    import torch.distributed as dist
+    from paper_2206_01288_b200 import _native as N
+    from paper_2206_01288_b200.costmodel import comm_cost_batch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    g, w = instance()
+    inst = N.instance_for(g, w, local)
+    L = N.lib()
+    P = ARGS.population
+    nbuf = 4  # 4 x P x 128 B rotating inputs: 512 MiB at P=2^20 (> 126 MB L2)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    pops = []
+    for _ in range(nbuf):
+        keys = torch.rand((P, 64), device=dev, generator=gen)
+        perm = torch.argsort(keys, dim=1).to(torch.int16).view(P, 8, 8)
+        pops.append(torch.sort(perm, dim=2).values.contiguous())
+    outs = [torch.empty(P, dtype=torch.float64, device=dev) for _ in range(3)]
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def step(i):
+        N.check(L.hs_eval_batch(inst.handle, pops[i % nbuf].data_ptr(), P, outs[0].data_ptr(), outs[1].data_ptr(),
+                                outs[2].data_ptr(), None, None, bad.data_ptr(), sp), "hs_eval_batch")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for i in range(ARGS.warmup):
+        step(i)
+    barrier()
+    assert int(bad.item()) == 0
+    # spot parity of the last warm-up output (full parity lives in tests/)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(ARGS.steps + 1)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev[0].record(stream)
+        for i in range(ARGS.steps):
+            step(i)
+            ev[i + 1].record(stream)
+        barrier()
+    launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(ARGS.steps)]
+    t_ms = ev[0].elapsed_time(ev[-1])
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    value = P * ARGS.steps * world / (t_ms / 1000.0)
+
+    # e2e through the C-ABI host-buffer entry point: pinned host layouts in,
+    # totals/datap/pipelinep out, H2D/D2H inside the timed region.
+    host_pop = [pops[i].cpu().pin_memory().numpy() for i in range(2)]
+    host_out = [torch.empty(P, dtype=torch.float64).pin_memory().numpy() for _ in range(3)]
+    inv = np.zeros(1, dtype=np.int32)
+
+    def e2e_step(i):
+        N.check(L.hs_eval_batch_host(inst.handle, host_pop[i % 2].ctypes.data, P, host_out[0].ctypes.data,
+                                     host_out[1].ctypes.data, host_out[2].ctypes.data, None, None, inv.ctypes.data),
+                "hs_eval_batch_host")
+
+    for i in range(ARGS.warmup):
+        e2e_step(i)
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(ARGS.steps):
+        e2e_step(i)
+    barrier()
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = P * ARGS.steps * world / float(e2e_s.item())
+    # public-API check: same numbers through comm_cost_batch on the host array
+    last = (ARGS.steps - 1) % 2
+    api = comm_cost_batch(g, host_pop[last][:4096], w)
+    assert np.array_equal(api["total"], host_out[0][:4096]), "public API disagrees with the C-ABI host path"
+
+    csum = clocks.summary()
+    sm_mhz = csum["sm_mhz"] or 1965.0
+    kern_ms = sum(launch_ms) / len(launch_ms)
+    achieved = SMEM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = SMEM_BYTES_PER_CLK_SM * sms * sm_mhz * 1e6 / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": ARGS.steps,
+        "warmup": ARGS.warmup, "ms_per_step": t_ms / ARGS.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: uniformly random balanced layouts (device RNG), reference case-5 generator matrix",
+        "config": {"workload": WORKLOAD, "population_per_gpu": P,
+                   "l2": f"{nbuf} rotating input populations of {P * 128 / 2**20:.0f} MiB (> 126 MB L2)",
+                   "parallelism": f"population sharded over {world} GPU(s), no data-path collective"},
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "per_eval_bytes": SMEM_BYTES_PER_EVAL, "kernel": "eval_warp_kernel", "kernel_ms": kern_ms,
+                     "peak_source": f"architectural 128 B/clk/SM x {sms} SMs at the {sm_mhz:.0f} MHz SM clock "
+                                    "sampled during this run (MEASURED_PEAKS.json has no smem figure)",
+                     "hbm_achieved_gbs": HBM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9},
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": P * 128, "d2h_bytes_per_step": P * 24,
+                "path": "hs_eval_batch_host (C-ABI, pinned host buffers)"},
+        "gpu_launches": ARGS.steps,
+        "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
+    }
+    if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
+        from oracle import oracle as O
+        threads = O.cpu_count()
+        rate, count, dt = cpu_oracle_rate(g, w, ARGS.cpu_seconds, threads)
+        line["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads, "kind": "port",
+                                "sample": f"{count} random 8x8 case-{ARGS.case} layouts in {dt:.1f} s "
+                                          f"(C oracle restatement of comm_cost, {threads} threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    ARGS = parse()
+    if ARGS.impl == "reference":
+        run_reference()
+    else:
+        run_ours()

@@ -1,0 +1,177 @@
+"""Bi-level communication cost of balanced partitions, evaluated on the GPU.
+
+Drop-in mirror of hetsched/costmodel.py's hot-path surface:
+``Partition`` (:47-95), ``CostBreakdown`` (:114-131), ``comm_cost``
+(:217-229), ``datap_cost`` (:171-175), ``pipeline_cost`` (:211-214), plus the
+batch entry point ``comm_cost_batch`` that the GPU path adds.  Every cost
+is computed by the sm_100a kernels in lib/libhetsched_sm100a.so (K0 pair
+tables + K1 warp-per-candidate evaluator); Python only validates, packs
+int16 layouts and unpacks results.  Results are bit-identical to the
+reference (tests/test_gpu_costmodel.py).
+
+Graphs and workloads are duck-typed: anything with ``lat``/``bw`` arrays and
+``d_pp``/``d_dp``/``c_pp``/``c_dp`` works, including the reference's own
+dataclasses.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterable
+
+import numpy as np
+
+from . import _native as N
+from .combinatorics import PathResult, open_loop_tsp
+from .workload import validate_workload
+
+
+class CostModelError(ValueError):
+    """Partition inconsistent with the network or the workload."""
+
+
+@dataclass(frozen=True)
+class Partition:
+    """Balanced partition of devices 0..N-1; members ascending, group order kept."""
+
+    groups: tuple[tuple[int, ...], ...]
+
+    def __post_init__(self) -> None:
+        groups = tuple(tuple(sorted(int(d) for d in grp)) for grp in self.groups)
+        if not groups or not groups[0]:
+            raise CostModelError("partition needs at least one non-empty group")
+        if len({len(g) for g in groups}) != 1:
+            raise CostModelError(f"unbalanced groups: sizes {sorted(len(g) for g in groups)}")
+        flat = sorted(d for g in groups for d in g)
+        if flat != list(range(len(flat))):
+            raise CostModelError("groups must be disjoint and cover devices 0..N-1 exactly")
+        object.__setattr__(self, "groups", groups)
+
+    @property
+    def d_pp(self) -> int:
+        return len(self.groups)
+
+    @property
+    def d_dp(self) -> int:
+        return len(self.groups[0])
+
+    @property
+    def n(self) -> int:
+        return self.d_pp * self.d_dp
+
+    def canonical(self) -> "Partition":
+        return Partition(tuple(sorted(self.groups)))
+
+    def key(self) -> tuple[tuple[int, ...], ...]:
+        return tuple(sorted(self.groups))
+
+    @classmethod
+    def from_groups(cls, groups: Iterable[Iterable[int]]) -> "Partition":
+        return cls(tuple(tuple(g) for g in groups))
+
+    def as_array(self) -> np.ndarray:
+        return np.asarray(self.groups, dtype=np.int16)
+
+
+@dataclass(frozen=True)
+class CostBreakdown:
+    datap: float
+    pipelinep: float
+    total: float
+    per_group_datap: tuple[float, ...]
+    pipeline_order: PathResult
+
+    def to_dict(self) -> dict:
+        return {
+            "datap": self.datap,
+            "pipelinep": self.pipelinep,
+            "total": self.total,
+            "per_group_datap": list(self.per_group_datap),
+            "pipeline_order": list(self.pipeline_order.order),
+        }
+
+
+def _check_partition(p, g, w) -> None:
+    n = len(p.groups) * len(p.groups[0])
+    if n != g.lat.shape[0]:
+        raise CostModelError(f"partition covers {n} devices but the network has {g.lat.shape[0]}")
+    if len(p.groups) != w.d_pp or len(p.groups[0]) != w.d_dp:
+        raise CostModelError(
+            f"partition shape {len(p.groups)}x{len(p.groups[0])} does not match workload {w.d_pp}x{w.d_dp}")
+
+
+def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = False, device: int | None = None):
+    """Costs of a batch of partitions in one GPU pass.
+
+    ``groups``: int16-compatible [P, d_pp, d_dp] with ascending members --
+    a numpy array (host path: pinned staging, chunked H2D / kernel / D2H
+    overlap) or a torch CUDA tensor (device path, current stream).
+    Returns a dict of arrays (numpy for host input, torch for device input):
+    total, datap, pipelinep and optionally per_group [P, d_pp], order [P, d_pp].
+    Malformed partitions raise CostModelError.
+    """
+    validate_workload(w, g.lat.shape[0])
+    inst = N.instance_for(g, w, device)
+    k = inst.k
+    if isinstance(groups, np.ndarray) or not hasattr(groups, "data_ptr"):
+        a = np.ascontiguousarray(groups, dtype=np.int16)
+        if a.ndim != 3 or a.shape[1:] != (inst.k, inst.m):
+            raise CostModelError(f"expected groups of shape [P, {inst.k}, {inst.m}], got {a.shape}")
+        P = a.shape[0]
+        out = {"total": np.empty(P), "datap": np.empty(P), "pipelinep": np.empty(P)}
+        if per_group:
+            out["per_group"] = np.empty((P, k))
+        if order:
+            out["order"] = np.empty((P, k), dtype=np.int8)
+        bad = np.zeros(1, dtype=np.int32)
+        N.check(N.lib().hs_eval_batch_host(inst.handle, a.ctypes.data, P, N.ptr(out["total"]), N.ptr(out["datap"]),
+                                           N.ptr(out["pipelinep"]), N.ptr(out.get("per_group")),
+                                           N.ptr(out.get("order")), bad.ctypes.data), "hs_eval_batch_host")
+        nbad = int(bad[0])
+    else:
+        torch = N.torch_cuda()
+        t = groups
+        if t.dtype != torch.int16 or not t.is_contiguous() or t.device.index != inst.device:
+            t = t.to(device=f"cuda:{inst.device}", dtype=torch.int16).contiguous()
+        if t.dim() != 3 or tuple(t.shape[1:]) != (inst.k, inst.m):
+            raise CostModelError(f"expected groups of shape [P, {inst.k}, {inst.m}], got {tuple(t.shape)}")
+        P = t.shape[0]
+        dev = f"cuda:{inst.device}"
+        out = {name: torch.empty(P, dtype=torch.float64, device=dev) for name in ("total", "datap", "pipelinep")}
+        if per_group:
+            out["per_group"] = torch.empty((P, k), dtype=torch.float64, device=dev)
+        if order:
+            out["order"] = torch.empty((P, k), dtype=torch.int8, device=dev)
+        bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        N.check(N.lib().hs_eval_batch(inst.handle, t.data_ptr(), P, out["total"].data_ptr(), out["datap"].data_ptr(),
+                                      out["pipelinep"].data_ptr(), N.ptr(out.get("per_group")),
+                                      N.ptr(out.get("order")), bad.data_ptr(), N.stream_ptr(inst.device)),
+                "hs_eval_batch")
+        nbad = int(bad.item())
+    if nbad:
+        raise CostModelError(
+            f"{nbad} of {P} partitions are not balanced partitions of 0..N-1 with ascending members")
+    return out
+
+
+def comm_cost(g, p, w, heuristic: bool = False) -> CostBreakdown:
+    """Full bi-level cost of one balanced partition (costmodel.py:217-229)."""
+    validate_workload(w, g.lat.shape[0])
+    _check_partition(p, g, w)
+    r = comm_cost_batch(g, np.asarray([p.groups], dtype=np.int16), w, per_group=True, order=True)
+    total, datap, pipe = float(r["total"][0]), float(r["datap"][0]), float(r["pipelinep"][0])
+    return CostBreakdown(datap=datap, pipelinep=pipe, total=total,
+                         per_group_datap=tuple(float(x) for x in r["per_group"][0]),
+                         pipeline_order=PathResult(tuple(int(x) for x in r["order"][0]), pipe))
+
+
+def datap_cost(g, p, w) -> tuple[float, tuple[float, ...]]:
+    """Data-parallel level: slowest group and the per-group values."""
+    _check_partition(p, g, w)
+    cb = comm_cost(g, p, w)
+    return cb.datap, cb.per_group_datap
+
+
+def pipeline_cost(cg, heuristic: bool = False) -> tuple[float, PathResult]:
+    """Cheapest open chain through a coarsened edge matrix (costmodel.py:211-214)."""
+    res = open_loop_tsp(cg.edge_cost if hasattr(cg, "edge_cost") else cg, heuristic=heuristic)
+    return res.total, res

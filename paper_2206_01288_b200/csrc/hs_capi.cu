@@ -1,0 +1,301 @@
+// hs_capi.cu -- the C-ABI (include/hetsched_b200.h) over the sm_100a kernels.
+#include <thrust/device_ptr.h>
+#include <thrust/execution_policy.h>
+#include <thrust/sort.h>
+#include <thrust/unique.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hetsched_b200.h"
+#include "hs_eval.cuh"
+#include "hs_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
+    char buf[512];
+    if (e != cudaSuccess)
+        snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+    else
+        snprintf(buf, sizeof buf, "%s", what);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call, what)                               \
+    do {                                             \
+        cudaError_t e_ = (call);                     \
+        if (e_ != cudaSuccess) return fail(-1, what, e_); \
+    } while (0)
+
+// Held-Karp states (s | u << 8) grouped by |s|, for k <= 8.
+void hk_states(int k, std::vector<uint16_t>& st, int off[18]) {
+    st.clear();
+    for (int i = 0; i < 18; i++) off[i] = 0;
+    for (int p = 0; p <= k + 1 && p < 18; p++) {
+        off[p] = (int)st.size();
+        if (p < 2 || p > k) continue;
+        for (int s = 0; s < (1 << k); s++) {
+            if (__builtin_popcount(s) != p) continue;
+            for (int u = 0; u < k; u++)
+                if (s >> u & 1) st.push_back((uint16_t)(s | (u << 8)));
+        }
+    }
+    for (int p = k + 1; p < 18; p++) off[p] = (int)st.size();
+}
+
+struct DeviceStates {
+    uint16_t* d = nullptr;
+    int n = 0;
+    int off[18];
+};
+
+std::mutex g_states_mu;
+std::map<std::pair<int, int>, DeviceStates> g_states;  // (device, k)
+
+int get_states(int device, int k, DeviceStates* out) {
+    std::lock_guard<std::mutex> lk(g_states_mu);
+    auto key = std::make_pair(device, k);
+    auto it = g_states.find(key);
+    if (it == g_states.end()) {
+        DeviceStates ds;
+        std::vector<uint16_t> st;
+        hk_states(k, st, ds.off);
+        ds.n = (int)st.size();
+        CK(cudaMalloc(&ds.d, std::max<size_t>(2, st.size() * 2)), "cudaMalloc states");
+        if (!st.empty()) CK(cudaMemcpy(ds.d, st.data(), st.size() * 2, cudaMemcpyHostToDevice), "upload states");
+        it = g_states.emplace(key, ds).first;
+    }
+    *out = it->second;
+    return 0;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace
+
+struct hs_instance {
+    int device = 0, n = 0, k = 0, m = 0, sm_count = 0;
+    size_t smem_optin = 0;
+    double *lat = nullptr, *bw = nullptr, *dp = nullptr, *pp = nullptr, *sw = nullptr, *vals = nullptr;
+    uint32_t* rank = nullptr;
+    int nvals = 0;
+    DeviceStates states;
+    int* invalid = nullptr;
+    hs::EvalPlan plan{};
+    // host-buffer path
+    std::mutex mu;
+    int64_t chunk = 0;
+    int16_t* cg[2] = {nullptr, nullptr};
+    double* co[2] = {nullptr, nullptr};
+    int* cinv = nullptr;
+    cudaStream_t cs[2] = {nullptr, nullptr};
+};
+
+static hs::EvalArgs base_args(const hs_instance* h) {
+    hs::EvalArgs a{};
+    a.n = h->n;
+    a.k = h->k;
+    a.m = h->m;
+    a.dp = h->dp;
+    a.rank = h->rank;
+    a.vals = h->vals;
+    a.states = h->states.d;
+    a.nstates = h->states.n;
+    for (int i = 0; i < 18; i++) a.off[i] = h->states.off[i];
+    return a;
+}
+
+extern "C" {
+
+int hs_version(void) { return 1; }
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+
+int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int d_dp, double dp_num,
+                       double pp_num, double sw_num, int device, hs_instance** out) {
+    if (!out || !lat || !bw) return fail(-2, "null argument");
+    if (n < 1 || d_pp < 1 || d_dp < 1 || (int64_t)d_pp * d_dp != n) return fail(-2, "d_pp*d_dp must equal n");
+    if (d_dp > hs::kMaxM) return fail(-3, "d_dp > 64 is not supported");
+    if (d_pp > hs::kWarpK) return fail(-3, "d_pp > 8 is not supported by the warp evaluator yet");
+    if (n > 32767) return fail(-3, "n > 32767 is not supported (int16 device ids)");
+    DeviceGuard dg(device);
+    hs_instance* h = new hs_instance();
+    h->device = device;
+    h->n = n;
+    h->k = d_pp;
+    h->m = d_dp;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    h->sm_count = prop.multiProcessorCount;
+    h->smem_optin = prop.sharedMemPerBlockOptin;
+    size_t nn = (size_t)n * n;
+    CK(cudaMalloc(&h->lat, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->bw, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->dp, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->pp, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->sw, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->vals, nn * 8), "cudaMalloc");
+    CK(cudaMalloc(&h->rank, nn * 4), "cudaMalloc");
+    CK(cudaMalloc(&h->invalid, sizeof(int)), "cudaMalloc");
+    CK(cudaMemcpy(h->lat, lat, nn * 8, cudaMemcpyHostToDevice), "upload lat");
+    CK(cudaMemcpy(h->bw, bw, nn * 8, cudaMemcpyHostToDevice), "upload bw");
+    if (hs::launch_build_tables(n, h->lat, h->bw, d_dp, dp_num, pp_num, sw_num, h->dp, h->pp, h->sw, 0))
+        return fail(-1, "build_tables launch");
+    CK(cudaMemcpy(h->vals, h->pp, nn * 8, cudaMemcpyDeviceToDevice), "copy pp");
+    thrust::device_ptr<double> v(h->vals);
+    thrust::sort(thrust::device, v, v + nn);
+    h->nvals = (int)(thrust::unique(thrust::device, v, v + nn) - v);
+    if (hs::launch_rank((int64_t)nn, h->pp, h->vals, h->nvals, h->rank, 0)) return fail(-1, "rank launch");
+    CK(cudaDeviceSynchronize(), "instance tables");
+    int rc = get_states(device, d_pp, &h->states);
+    if (rc) return rc;
+    hs::EvalArgs a = base_args(h);
+    if (hs::eval_plan(a, h->sm_count, h->smem_optin, &h->plan)) return fail(-3, "shape does not fit shared memory");
+    *out = h;
+    return 0;
+}
+
+int hs_instance_destroy(hs_instance* h) {
+    if (!h) return 0;
+    DeviceGuard dg(h->device);
+    cudaFree(h->lat);
+    cudaFree(h->bw);
+    cudaFree(h->dp);
+    cudaFree(h->pp);
+    cudaFree(h->sw);
+    cudaFree(h->vals);
+    cudaFree(h->rank);
+    cudaFree(h->invalid);
+    for (int i = 0; i < 2; i++) {
+        if (h->cg[i]) cudaFree(h->cg[i]);
+        if (h->co[i]) cudaFree(h->co[i]);
+        if (h->cs[i]) cudaStreamDestroy(h->cs[i]);
+    }
+    if (h->cinv) cudaFree(h->cinv);
+    delete h;
+    return 0;
+}
+
+int hs_instance_tables(hs_instance* h, double* dp, double* pp, double* sw) {
+    if (!h) return fail(-2, "null handle");
+    DeviceGuard dg(h->device);
+    size_t nn = (size_t)h->n * h->n * 8;
+    if (dp) CK(cudaMemcpy(dp, h->dp, nn, cudaMemcpyDeviceToHost), "download dp");
+    if (pp) CK(cudaMemcpy(pp, h->pp, nn, cudaMemcpyDeviceToHost), "download pp");
+    if (sw) CK(cudaMemcpy(sw, h->sw, nn, cudaMemcpyDeviceToHost), "download sw");
+    return 0;
+}
+
+int hs_eval_batch(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
+                  double* pipelinep, double* per_group, int8_t* order, int32_t* invalid, void* stream) {
+    if (!h) return fail(-2, "null handle");
+    if (P < 0) return fail(-2, "negative batch");
+    if (P == 0) return 0;
+    if (!groups || !total) return fail(-2, "null buffer");
+    DeviceGuard dg(h->device);
+    hs::EvalArgs a = base_args(h);
+    a.groups = groups;
+    a.P = P;
+    a.total = total;
+    a.datap = datap;
+    a.pipe = pipelinep;
+    a.per_group = per_group;
+    a.order = order;
+    a.invalid = invalid ? invalid : h->invalid;
+    if (hs::launch_eval(a, h->plan, (cudaStream_t)stream)) return fail(-1, "eval launch", cudaGetLastError());
+    return 0;
+}
+
+int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
+                       double* pipelinep, double* per_group, int8_t* order, int32_t* invalid) {
+    if (!h) return fail(-2, "null handle");
+    if (P < 0) return fail(-2, "negative batch");
+    if (invalid) *invalid = 0;
+    if (P == 0) return 0;
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard dg(h->device);
+    const int km = h->k * h->m;
+    if (!h->chunk) {
+        h->chunk = 1 << 18;
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMalloc(&h->cg[i], (size_t)h->chunk * km * 2), "cudaMalloc chunk");
+            CK(cudaMalloc(&h->co[i], (size_t)h->chunk * (3 + h->k) * 8 + (size_t)h->chunk * h->k), "cudaMalloc chunk");
+            CK(cudaStreamCreateWithFlags(&h->cs[i], cudaStreamNonBlocking), "stream");
+        }
+        CK(cudaMalloc(&h->cinv, sizeof(int)), "cudaMalloc");
+    }
+    CK(cudaMemsetAsync(h->cinv, 0, sizeof(int), h->cs[0]), "memset");
+    CK(cudaStreamSynchronize(h->cs[0]), "sync");
+    hs::EvalArgs a = base_args(h);
+    a.invalid = h->cinv;
+    int64_t nchunks = (P + h->chunk - 1) / h->chunk;
+    for (int64_t c = 0; c < nchunks; c++) {
+        int b = (int)(c & 1);
+        cudaStream_t s = h->cs[b];
+        int64_t lo = c * h->chunk, cnt = std::min<int64_t>(h->chunk, P - lo);
+        CK(cudaMemcpyAsync(h->cg[b], groups + lo * km, (size_t)cnt * km * 2, cudaMemcpyHostToDevice, s), "H2D");
+        a.groups = h->cg[b];
+        a.P = cnt;
+        a.total = h->co[b];
+        a.datap = h->co[b] + h->chunk;
+        a.pipe = h->co[b] + 2 * h->chunk;
+        a.per_group = per_group ? h->co[b] + 3 * h->chunk : nullptr;
+        a.order = order ? reinterpret_cast<int8_t*>(h->co[b] + (3 + h->k) * h->chunk) : nullptr;
+        if (hs::launch_eval(a, h->plan, s)) return fail(-1, "eval launch", cudaGetLastError());
+        CK(cudaMemcpyAsync(total + lo, a.total, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (datap) CK(cudaMemcpyAsync(datap + lo, a.datap, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (pipelinep) CK(cudaMemcpyAsync(pipelinep + lo, a.pipe, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+        if (per_group)
+            CK(cudaMemcpyAsync(per_group + lo * h->k, a.per_group, (size_t)cnt * h->k * 8, cudaMemcpyDeviceToHost, s),
+               "D2H");
+        if (order) CK(cudaMemcpyAsync(order + lo * h->k, a.order, (size_t)cnt * h->k, cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    CK(cudaStreamSynchronize(h->cs[0]), "sync");
+    CK(cudaStreamSynchronize(h->cs[1]), "sync");
+    if (invalid) CK(cudaMemcpy(invalid, h->cinv, sizeof(int), cudaMemcpyDeviceToHost), "D2H invalid");
+    return 0;
+}
+
+int hs_bottleneck_batch(const double* w, int m, int64_t B, double* out, int device, void* stream) {
+    if (m < 1 || m > hs::kMaxM) return fail(-3, "bottleneck: m must be in 1..64");
+    DeviceGuard dg(device);
+    if (hs::launch_bottleneck_batch(w, m, B, out, (cudaStream_t)stream))
+        return fail(-1, "bottleneck launch", cudaGetLastError());
+    return 0;
+}
+
+int hs_path_batch(const double* w, int k, int64_t B, double* total, int8_t* order, int device, void* stream) {
+    if (k < 1 || k > hs::kWarpK) return fail(-3, "path: k must be in 1..8");
+    DeviceGuard dg(device);
+    DeviceStates ds;
+    int rc = get_states(device, k, &ds);
+    if (rc) return rc;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "props");
+    hs::PathOff po;
+    for (int i = 0; i < 18; i++) po.off[i] = ds.off[i];
+    if (hs::launch_path_batch(w, k, B, ds.d, ds.n, po, total, order, prop.multiProcessorCount, (cudaStream_t)stream))
+        return fail(-1, "path launch", cudaGetLastError());
+    return 0;
+}
+
+}  // extern "C"

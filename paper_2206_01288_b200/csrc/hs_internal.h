@@ -1,0 +1,45 @@
+// hs_internal.h -- host-side declarations shared by the kernels and the C-ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hs {
+
+struct EvalArgs {
+    int n, k, m;
+    const double* dp;      // n*n data-parallel pair seconds (0 diagonal)
+    const uint32_t* rank;  // n*n rank of PP entries among distinct values
+    const double* vals;    // distinct PP values, ascending
+    const uint16_t* states;
+    int nstates;
+    int off[18];
+    const int16_t* groups;  // [P][k][m], members ascending
+    int64_t P;
+    double* total;
+    double* datap;
+    double* pipe;
+    double* per_group;  // [P][k] or null
+    int8_t* order;      // [P][k] or null
+    int* invalid;       // count of malformed candidates
+};
+
+struct EvalPlan {
+    bool smem_tables;
+    int warps, blocks;
+    size_t smem;
+};
+
+struct PathOff {
+    int off[18];
+};
+
+int launch_build_tables(int n, const double* lat, const double* bw, int d_dp, double dp_num, double pp_num,
+                        double sw_num, double* dp, double* pp, double* sw, cudaStream_t s);
+int launch_rank(int64_t nn, const double* pp, const double* vals, int nvals, uint32_t* rank, cudaStream_t s);
+int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan);
+int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s);
+int launch_bottleneck_batch(const double* w, int m, int64_t B, double* out, cudaStream_t s);
+int launch_path_batch(const double* w, int k, int64_t B, const uint16_t* states, int nstates, const PathOff& po,
+                      double* total, int8_t* order, int sm_count, cudaStream_t s);
+
+}  // namespace hs

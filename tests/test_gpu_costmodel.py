@@ -1,0 +1,169 @@
+"""GPU parity of the fitness evaluator (K0 tables + K1 eval) through the C-ABI.
+
+Every comparison is bitwise (==) against the oracle or against the golden
+vectors the reference produced; no tolerance is applied anywhere.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import _instances as I
+
+pytestmark = pytest.mark.gpu
+
+hs = pytest.importorskip("paper_2206_01288_b200")
+
+
+def _gpu_names():
+    return [n for n, m in I.meta().items() if m["recipe"]["w"][0] <= 8 and m["recipe"]["w"][1] <= 64]
+
+
+@pytest.mark.parametrize("name", sorted(_gpu_names()))
+def test_pair_tables_bitwise(name):
+    from paper_2206_01288_b200 import _native as N
+    g, w = I.instance(name)
+    dp, pp, sw = N.instance_for(g, w).tables()
+    odp, opp, osw = O.Oracle.of(g, w).tables()
+    assert np.array_equal(dp, odp) and np.array_equal(pp, opp) and np.array_equal(sw, osw)
+
+
+@pytest.mark.parametrize("name", sorted(_gpu_names()))
+def test_batch_matches_reference_golden(name):
+    g, w = I.instance(name)
+    C = I.costs()
+    parts = C[f"{name}/parts"]
+    r = hs.comm_cost_batch(g, parts, w, per_group=True, order=True)
+    assert np.array_equal(r["total"], C[f"{name}/total"])
+    assert np.array_equal(r["datap"], C[f"{name}/datap"])
+    assert np.array_equal(r["pipelinep"], C[f"{name}/pipelinep"])
+    assert np.array_equal(r["per_group"], C[f"{name}/per_group"])
+    assert np.array_equal(r["order"].astype(np.int16), C[f"{name}/order"])
+
+
+def test_single_comm_cost_breakdown():
+    g, w = I.instance("case5")
+    C = I.costs()
+    for i in range(5):
+        p = hs.Partition.from_groups(C["case5/parts"][i].tolist())
+        cb = hs.comm_cost(g, p, w)
+        assert cb.total == C["case5/total"][i]
+        assert cb.total == cb.datap + cb.pipelinep
+        assert cb.per_group_datap == tuple(C["case5/per_group"][i])
+        assert cb.pipeline_order.order == tuple(int(x) for x in C["case5/order"][i])
+        assert cb.pipeline_order.total == cb.pipelinep
+
+
+def test_g4_golden_values():
+    g, w = I.instance("g4")
+    good = hs.comm_cost(g, hs.Partition(((0, 1), (2, 3))), w)
+    assert good.datap == 0.402 and good.pipelinep == 2.1
+    assert good.total == pytest.approx(2.502, rel=1e-9)
+    for p in (((0, 2), (1, 3)), ((0, 3), (1, 2))):
+        bad = hs.comm_cost(g, hs.Partition(p), w)
+        assert bad.datap == 4.1 and bad.pipelinep == 0.202
+
+
+def _random_parts(seed, count, n, k, m):
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.permuted(np.tile(np.arange(n, dtype=np.int16), (count, 1)), axis=1).reshape(count, k, m),
+                   axis=2)
+
+
+@pytest.mark.parametrize("case", [1, 2, 3, 4, 5])
+def test_20k_layouts_per_case_bitwise_vs_oracle(case):
+    g, w = I.instance(f"case{case}")
+    parts = _random_parts(case, 20000, 64, 8, 8)
+    r = hs.comm_cost_batch(g, parts, w)
+    t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"], t)
+    assert np.array_equal(r["datap"], d)
+    assert np.array_equal(r["pipelinep"], p)
+
+
+@pytest.mark.parametrize("name", ["r64_8x8", "r36_6x6", "r64_2x32", "r48_3x16", "r40_4x10", "config1"])
+def test_random_graphs_bitwise_vs_oracle(name):
+    g, w = I.instance(name)
+    parts = _random_parts(7, 3000, g.n, w.d_pp, w.d_dp)
+    r = hs.comm_cost_batch(g, parts, w)
+    t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"], t) and np.array_equal(r["datap"], d) and np.array_equal(r["pipelinep"], p)
+
+
+def test_device_tensor_path_matches_host_path():
+    import torch
+    g, w = I.instance("case4")
+    parts = _random_parts(11, 4096, 64, 8, 8)
+    host = hs.comm_cost_batch(g, parts, w, per_group=True, order=True)
+    dev = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w, per_group=True, order=True)
+    for key in host:
+        assert np.array_equal(host[key], dev[key].cpu().numpy()), key
+
+
+def test_relabeling_groups_is_invariant_at_scale():
+    g, w = I.instance("case5")
+    parts = _random_parts(3, 8192, 64, 8, 8)
+    rng = np.random.default_rng(0)
+    shuffled = np.stack([p[rng.permutation(8)] for p in parts])
+    a = hs.comm_cost_batch(g, parts, w)
+    b = hs.comm_cost_batch(g, shuffled, w)
+    for key in a:
+        assert np.array_equal(a[key], b[key])
+
+
+def test_chunked_host_path_crosses_chunk_boundary():
+    g, w = I.instance("case2")
+    parts = _random_parts(5, (1 << 18) + 1000, 64, 8, 8)
+    r = hs.comm_cost_batch(g, parts, w)
+    sel = np.r_[0:50, (1 << 18) - 25:(1 << 18) + 25, len(parts) - 50:len(parts)]
+    t, _, _ = O.Oracle.of(g, w).comm_cost_batch(parts[sel], threads=O.cpu_count())
+    assert np.array_equal(r["total"][sel], t)
+    assert np.all(np.isfinite(r["total"]))
+
+
+def test_malformed_partitions_raise():
+    g, w = I.instance("case1")
+    parts = _random_parts(1, 64, 64, 8, 8)
+    bad = parts.copy()
+    bad[3, 0, 0] = bad[3, 1, 0]  # duplicate device
+    with pytest.raises(hs.CostModelError, match="1 of 64"):
+        hs.comm_cost_batch(g, bad, w)
+    bad = parts.copy()
+    bad[5, 2] = bad[5, 2][::-1]  # descending members
+    with pytest.raises(hs.CostModelError):
+        hs.comm_cost_batch(g, bad, w)
+    bad = parts.copy()
+    bad[7, 0, 0] = 64  # out of range
+    with pytest.raises(hs.CostModelError):
+        hs.comm_cost_batch(g, bad, w)
+
+
+def test_empty_batch():
+    g, w = I.instance("case1")
+    r = hs.comm_cost_batch(g, np.empty((0, 8, 8), dtype=np.int16), w)
+    assert r["total"].shape == (0,)
+
+
+def test_bottleneck_and_path_solvers_vs_golden():
+    fxs = I.fixture("solvers.json")
+    for c in fxs["matching"]:
+        m = c["m"]
+        wm = np.array([I.fx(x) for x in c["w"]]).reshape(m, m)
+        assert hs.bottleneck_value(wm) == I.fx(c["value"])
+    for c in fxs["tsp"]:
+        k = c["k"]
+        if k > 8:
+            continue
+        wm = np.array([I.fx(x) for x in c["w"]]).reshape(k, k)
+        r = hs.open_loop_tsp(wm)
+        assert r.total == I.fx(c["total"]) and list(r.order) == c["order"]
+
+
+def test_batched_bottleneck_vs_oracle_with_ties():
+    rng = np.random.default_rng(9)
+    for m in (1, 2, 3, 5, 8, 13, 32, 64):
+        stack = rng.integers(0, 6, size=(300, m, m)).astype(float) * 0.25
+        got = hs.bottleneck_values(stack)
+        want = np.array([O.bottleneck_value(x) for x in stack])
+        assert np.array_equal(got, want), m
