@@ -35,45 +35,64 @@ int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
         if (e_ != cudaSuccess) return fail(-1, what, e_); \
     } while (0)
 
-// Held-Karp states (s | u << 8) grouped by |s|, for k <= 8.
-void hk_states(int k, std::vector<uint16_t>& st, int off[18]) {
+// Held-Karp schedule for k <= 8 (see hs_eval.cuh, warp_held_karp): compact
+// offsets off[s] (entries for |s| >= 2, s ascending), and per state (s, u)
+// the word off[r] | dst << 10 | u << 20 | r << 23 with r = s \ u, grouped by
+// layer |s|.
+void hk_schedule(int k, std::vector<uint32_t>& st, std::vector<uint16_t>& hoff, int lay[18]) {
     st.clear();
-    for (int i = 0; i < 18; i++) off[i] = 0;
-    for (int p = 0; p <= k + 1 && p < 18; p++) {
-        off[p] = (int)st.size();
+    hoff.assign((size_t)1 << k, 0);
+    int acc = 0;
+    for (int s = 0; s < (1 << k); s++) {
+        hoff[s] = (uint16_t)acc;
+        if (__builtin_popcount(s) >= 2) acc += __builtin_popcount(s);
+    }
+    for (int i = 0; i < 18; i++) lay[i] = 0;
+    for (int p = 0; p < 18; p++) {
+        lay[p] = (int)st.size();
         if (p < 2 || p > k) continue;
         for (int s = 0; s < (1 << k); s++) {
             if (__builtin_popcount(s) != p) continue;
-            for (int u = 0; u < k; u++)
-                if (s >> u & 1) st.push_back((uint16_t)(s | (u << 8)));
+            for (int u = 0; u < k; u++) {
+                if (!(s >> u & 1)) continue;
+                int r = s ^ (1 << u);
+                uint32_t dst = hoff[s] + __builtin_popcount(s & ((1 << u) - 1));
+                uint32_t offr = __builtin_popcount(r) >= 2 ? hoff[r] : 0;
+                st.push_back(offr | (dst << 10) | ((uint32_t)u << 20) | ((uint32_t)r << 23));
+            }
         }
     }
-    for (int p = k + 1; p < 18; p++) off[p] = (int)st.size();
 }
 
-struct DeviceStates {
-    uint16_t* d = nullptr;
-    int n = 0;
-    int off[18];
+struct DeviceHK {
+    uint32_t* st = nullptr;
+    uint16_t* hoff = nullptr;
+    hs::HKTables t{};
 };
 
-std::mutex g_states_mu;
-std::map<std::pair<int, int>, DeviceStates> g_states;  // (device, k)
+std::mutex g_hk_mu;
+std::map<std::pair<int, int>, DeviceHK> g_hk;  // (device, k)
 
-int get_states(int device, int k, DeviceStates* out) {
-    std::lock_guard<std::mutex> lk(g_states_mu);
+int get_hk(int device, int k, hs::HKTables* out) {
+    std::lock_guard<std::mutex> lk(g_hk_mu);
     auto key = std::make_pair(device, k);
-    auto it = g_states.find(key);
-    if (it == g_states.end()) {
-        DeviceStates ds;
-        std::vector<uint16_t> st;
-        hk_states(k, st, ds.off);
-        ds.n = (int)st.size();
-        CK(cudaMalloc(&ds.d, std::max<size_t>(2, st.size() * 2)), "cudaMalloc states");
-        if (!st.empty()) CK(cudaMemcpy(ds.d, st.data(), st.size() * 2, cudaMemcpyHostToDevice), "upload states");
-        it = g_states.emplace(key, ds).first;
+    auto it = g_hk.find(key);
+    if (it == g_hk.end()) {
+        DeviceHK d;
+        std::vector<uint32_t> st;
+        std::vector<uint16_t> hoff;
+        hk_schedule(k, st, hoff, d.t.lay);
+        CK(cudaMalloc(&d.st, std::max<size_t>(4, st.size() * 4)), "cudaMalloc hk");
+        CK(cudaMalloc(&d.hoff, hoff.size() * 2), "cudaMalloc hk");
+        if (!st.empty()) CK(cudaMemcpy(d.st, st.data(), st.size() * 4, cudaMemcpyHostToDevice), "upload hk");
+        CK(cudaMemcpy(d.hoff, hoff.data(), hoff.size() * 2, cudaMemcpyHostToDevice), "upload hk");
+        d.t.states = d.st;
+        d.t.nstates = (int)st.size();
+        d.t.hoff = d.hoff;
+        d.t.nhoff = (int)hoff.size();
+        it = g_hk.emplace(key, d).first;
     }
-    *out = it->second;
+    *out = it->second.t;
     return 0;
 }
 
@@ -97,8 +116,9 @@ struct hs_instance {
     size_t smem_optin = 0;
     double *lat = nullptr, *bw = nullptr, *dp = nullptr, *pp = nullptr, *sw = nullptr, *vals = nullptr;
     uint32_t* rank = nullptr;
+    uint16_t* rank16 = nullptr;
     int nvals = 0;
-    DeviceStates states;
+    hs::HKTables hk{};
     int* invalid = nullptr;
     hs::EvalPlan plan{};
     // host-buffer path
@@ -116,11 +136,11 @@ static hs::EvalArgs base_args(const hs_instance* h) {
     a.k = h->k;
     a.m = h->m;
     a.dp = h->dp;
-    a.rank = h->rank;
+    a.key16 = h->rank16 != nullptr;
+    a.rank = a.key16 ? (const void*)h->rank16 : (const void*)h->rank;
+    a.nvals = h->nvals;
     a.vals = h->vals;
-    a.states = h->states.d;
-    a.nstates = h->states.n;
-    for (int i = 0; i < 18; i++) a.off[i] = h->states.off[i];
+    a.hk = h->hk;
     return a;
 }
 
@@ -165,8 +185,12 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
     thrust::sort(thrust::device, v, v + nn);
     h->nvals = (int)(thrust::unique(thrust::device, v, v + nn) - v);
     if (hs::launch_rank((int64_t)nn, h->pp, h->vals, h->nvals, h->rank, 0)) return fail(-1, "rank launch");
+    if (h->nvals <= 0xFFFF) {
+        CK(cudaMalloc(&h->rank16, nn * 2), "cudaMalloc");
+        if (hs::launch_narrow((int64_t)nn, h->rank, h->rank16, 0)) return fail(-1, "narrow launch");
+    }
     CK(cudaDeviceSynchronize(), "instance tables");
-    int rc = get_states(device, d_pp, &h->states);
+    int rc = get_hk(device, d_pp, &h->hk);
     if (rc) return rc;
     hs::EvalArgs a = base_args(h);
     if (hs::eval_plan(a, h->sm_count, h->smem_optin, &h->plan)) return fail(-3, "shape does not fit shared memory");
@@ -184,6 +208,7 @@ int hs_instance_destroy(hs_instance* h) {
     cudaFree(h->sw);
     cudaFree(h->vals);
     cudaFree(h->rank);
+    if (h->rank16) cudaFree(h->rank16);
     cudaFree(h->invalid);
     for (int i = 0; i < 2; i++) {
         if (h->cg[i]) cudaFree(h->cg[i]);
@@ -286,14 +311,21 @@ int hs_bottleneck_batch(const double* w, int m, int64_t B, double* out, int devi
 int hs_path_batch(const double* w, int k, int64_t B, double* total, int8_t* order, int device, void* stream) {
     if (k < 1 || k > hs::kWarpK) return fail(-3, "path: k must be in 1..8");
     DeviceGuard dg(device);
-    DeviceStates ds;
-    int rc = get_states(device, k, &ds);
+    if (k == 1) {
+        // a single vertex: empty path (combinatorics.py:241-242)
+        std::vector<double> z((size_t)B, 0.0);
+        std::vector<int8_t> o((size_t)B, 0);
+        CK(cudaMemcpyAsync(total, z.data(), (size_t)B * 8, cudaMemcpyHostToDevice, (cudaStream_t)stream), "H2D");
+        if (order) CK(cudaMemcpyAsync(order, o.data(), (size_t)B, cudaMemcpyHostToDevice, (cudaStream_t)stream), "H2D");
+        CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+        return 0;
+    }
+    hs::HKTables t;
+    int rc = get_hk(device, k, &t);
     if (rc) return rc;
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device), "props");
-    hs::PathOff po;
-    for (int i = 0; i < 18; i++) po.off[i] = ds.off[i];
-    if (hs::launch_path_batch(w, k, B, ds.d, ds.n, po, total, order, prop.multiProcessorCount, (cudaStream_t)stream))
+    if (hs::launch_path_batch(w, k, B, t, total, order, prop.multiProcessorCount, (cudaStream_t)stream))
         return fail(-1, "path launch", cudaGetLastError());
     return 0;
 }

@@ -21,7 +21,6 @@ namespace hs {
 
 constexpr int kMaxM = 64;     // uint64 masks
 constexpr int kWarpK = 8;     // warp kernel handles d_pp <= 8
-constexpr int kHS = 8;        // HK row stride (u index)
 
 // R(r, c) returns an ordered key (rank or value) of entry (r, c).
 template <typename Key, typename At>
@@ -99,48 +98,185 @@ __device__ Key bottleneck_threshold(int m, const At& R, Key key_max) {
     return L;
 }
 
-// Held-Karp over E (k x k, row stride kHS) by one warp.  h: 2^k * kHS
-// doubles (layers >= 2 written; layer 1 is implicit 0.0).  states:
-// (s | u << 8) grouped by |s|, layer p in [off[p], off[p+1]).
-__device__ __forceinline__ double hk_value(const double* h, int s, int u) {
-    return (s & (s - 1)) == 0 ? 0.0 : h[s * kHS + u];
+// ---------------------------------------------------------------------------
+// 8 x 8 bottleneck matching, register resident.
+//
+// K[r][q] packs the uint16 keys of columns q (low half) and q+4 (high half)
+// of row r; keys must be < 0x8000.  Adjacency at threshold L is one uint64
+// (bit 8r+c), built branch-free: per half, (0x8000|L) - key has bit 15 set
+// iff key <= L, and never borrows across halves.  Matching state lives in
+// packed 4-bit fields (0xF = free).
+struct Match8 {
+    __device__ __forceinline__ static uint32_t get4(uint32_t x, int i) { return (x >> (4 * i)) & 0xFu; }
+    __device__ __forceinline__ static uint32_t set4(uint32_t x, int i, uint32_t v) {
+        return (x & ~(0xFu << (4 * i))) | (v << (4 * i));
+    }
+
+    __device__ __forceinline__ static uint64_t adjacency(const uint32_t (&K)[8][4], uint32_t L) {
+        const uint32_t Lp = (L | (L << 16)) | 0x80008000u;
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            uint32_t t = ((Lp - K[r][0]) >> 15) & 0x00010001u;
+            t |= ((Lp - K[r][1]) >> 14) & 0x00020002u;
+            t |= ((Lp - K[r][2]) >> 13) & 0x00040004u;
+            t |= ((Lp - K[r][3]) >> 12) & 0x00080008u;
+            uint32_t row = (t | (t >> 12)) & 0xFFu;
+            if (r < 4)
+                lo |= row << (8 * r);
+            else
+                hi |= row << (8 * (r - 4));
+        }
+        return ((uint64_t)hi << 32) | lo;
+    }
+
+    __device__ static uint32_t solve(const uint32_t (&K)[8][4]) {
+        // lower bound: every row and every column needs one selected entry
+        uint32_t cm0 = 0xFFFFFFFFu, cm1 = 0xFFFFFFFFu, cm2 = 0xFFFFFFFFu, cm3 = 0xFFFFFFFFu;
+        uint32_t L = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            uint32_t t = __vminu2(__vminu2(K[r][0], K[r][1]), __vminu2(K[r][2], K[r][3]));
+            L = max(L, min(t & 0xFFFFu, t >> 16));
+            cm0 = __vminu2(cm0, K[r][0]);
+            cm1 = __vminu2(cm1, K[r][1]);
+            cm2 = __vminu2(cm2, K[r][2]);
+            cm3 = __vminu2(cm3, K[r][3]);
+        }
+        uint32_t c2 = __vmaxu2(__vmaxu2(cm0, cm1), __vmaxu2(cm2, cm3));
+        L = max(L, max(c2 & 0xFFFFu, c2 >> 16));
+        uint64_t adj = adjacency(K, L);
+        uint32_t mrow = 0xFFFFFFFFu, mcol = 0xFFFFFFFFu, used = 0, unmatched = 0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            uint32_t av = (uint32_t)(adj >> (8 * r)) & 0xFFu & ~used;
+            if (av) {
+                uint32_t c = __ffs(av) - 1;
+                used |= 1u << c;
+                mrow = set4(mrow, r, c);
+                mcol = set4(mcol, c, r);
+            } else {
+                unmatched |= 1u << r;
+            }
+        }
+        while (unmatched) {
+            int u = __ffs(unmatched) - 1;
+            unmatched &= unmatched - 1;
+            uint32_t rows_in = 1u << u, cols_in = 0, frontier = rows_in, parent = 0;
+            int found = -1;
+            for (;;) {
+                while (frontier && found < 0) {
+                    int r = __ffs(frontier) - 1;
+                    frontier &= frontier - 1;
+                    uint32_t cand = (uint32_t)(adj >> (8 * r)) & 0xFFu & ~cols_in;
+                    while (cand) {
+                        int c = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        parent = set4(parent, c, (uint32_t)r);
+                        cols_in |= 1u << c;
+                        uint32_t rr = get4(mcol, c);
+                        if (rr == 0xFu) {
+                            found = c;
+                            break;
+                        }
+                        rows_in |= 1u << rr;
+                        frontier |= 1u << rr;
+                    }
+                }
+                if (found >= 0) break;
+                // Hall violator: the optimum needs an edge leaving the tree;
+                // raise L to the cheapest such edge.
+                uint32_t M[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    M[q] = ((cols_in >> q) & 1u ? 0x0000FFFFu : 0u) | ((cols_in >> (q + 4)) & 1u ? 0xFFFF0000u : 0u);
+                uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    uint32_t t = __vminu2(__vminu2(K[r][0] | M[0], K[r][1] | M[1]),
+                                          __vminu2(K[r][2] | M[2], K[r][3] | M[3]));
+                    acc = __vminu2(acc, (rows_in >> r) & 1u ? t : 0xFFFFFFFFu);
+                }
+                L = min(acc & 0xFFFFu, acc >> 16);
+                adj = adjacency(K, L);
+                frontier = rows_in;
+            }
+            int c = found;
+            for (;;) {
+                int r = (int)get4(parent, c);
+                uint32_t pc = get4(mrow, r);
+                mrow = set4(mrow, r, (uint32_t)c);
+                mcol = set4(mcol, c, (uint32_t)r);
+                if (r == u) break;
+                c = (int)pc;
+            }
+        }
+        return L;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Held-Karp over E (k x k, row stride kES) by one warp, k <= 8.
+//
+// Compact table: h[off[s] + rank(u in s)] for u in s, |s| >= 2 (layer 1 is
+// implicit 0.0).  Iterating v over the bits of r = s\u in ascending order
+// visits h[off[r] + i] at consecutive i, so the h address is base + const.
+// Each state word: off[r] (bits 0-9) | dst index (10-19) | u (20-22) | r (23-30).
+// Layers p = |s| live in [lay[p], lay[p+1]).
+constexpr int kES = 9;  // padded E row stride (bank spread)
+
+template <int NV>
+__device__ __forceinline__ double hk_relax(const double* __restrict__ Eu, const double* __restrict__ hr, uint32_t r) {
+    double best = kInf;
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        int v = __ffs(r) - 1;
+        r &= r - 1;
+        double c = Eu[v] + hr[i];
+        best = c < best ? c : best;
+    }
+    return best;
 }
 
-__device__ inline double warp_held_karp(int k, const double* E, double* h, const uint16_t* states,
-                                        const int* off, int lane) {
+__device__ inline double warp_held_karp(int k, const double* E, double* h, const uint32_t* states, const int* lay,
+                                        int lane) {
     if (k == 1) return 0.0;
     for (int p = 2; p <= k; p++) {
-        for (int idx = off[p] + lane; idx < off[p + 1]; idx += kWarp) {
-            uint32_t st = states[idx];
-            int s = st & 0xff, u = st >> 8;
-            int r = s ^ (1 << u);
-            const double* Eu = E + u * kHS;
+        for (int idx = lay[p] + lane; idx < lay[p + 1]; idx += kWarp) {
+            uint32_t w = states[idx];
+            uint32_t r = w >> 23;
+            int u = (w >> 20) & 7;
+            const double* Eu = E + u * kES;
+            const double* hr = h + (w & 0x3FF);
             double best;
-            if (p == 2) {
-                best = Eu[__ffs(r) - 1];  // w[u][v] + 0.0 == w[u][v]
-            } else {
-                best = kInf;
-                const double* hr = h + r * kHS;
-                int rr = r;
-                while (rr) {
-                    int v = __ffs(rr) - 1;
-                    rr &= rr - 1;
-                    double c = Eu[v] + hr[v];
-                    best = c < best ? c : best;
-                }
+            switch (p) {
+                case 2: best = Eu[__ffs(r) - 1]; break;  // w[u][v] + 0.0 == w[u][v]
+                case 3: best = hk_relax<2>(Eu, hr, r); break;
+                case 4: best = hk_relax<3>(Eu, hr, r); break;
+                case 5: best = hk_relax<4>(Eu, hr, r); break;
+                case 6: best = hk_relax<5>(Eu, hr, r); break;
+                case 7: best = hk_relax<6>(Eu, hr, r); break;
+                default: best = hk_relax<7>(Eu, hr, r); break;
             }
-            h[s * kHS + u] = best;
+            h[(w >> 10) & 0x3FF] = best;
         }
         __syncwarp();
     }
-    int full = (1 << k) - 1;
-    double tot = h[full * kHS];
-    for (int u = 1; u < k; u++) tot = dmin(tot, h[full * kHS + u]);
+    // the full set's k entries are the last of the k*2^(k-1) - k slots
+    const double* hf = h + (k << (k - 1)) - 2 * k;
+    double tot = hf[0];
+    for (int u = 1; u < k; u++) tot = dmin(tot, hf[u]);
     return tot;
 }
 
+// compact index of (s, u), u in s, |s| >= 2
+__device__ __forceinline__ double hk_at(const double* h, const uint16_t* hoff, int s, int u) {
+    if ((s & (s - 1)) == 0) return 0.0;
+    return h[hoff[s] + __popc(s & ((1 << u) - 1))];
+}
+
 // Lexicographically smallest optimal walk (combinatorics.py:277-296).
-__device__ inline void held_karp_order(int k, const double* E, const double* h, double total,
+__device__ inline void held_karp_order(int k, const double* E, const double* h, const uint16_t* hoff, double total,
                                        int8_t* order) {
     if (k == 1) {
         order[0] = 0;
@@ -148,7 +284,7 @@ __device__ inline void held_karp_order(int k, const double* E, const double* h, 
     }
     int full = (1 << k) - 1;
     int start = 0;
-    while (h[full * kHS + start] != total) start++;
+    while (start < k - 1 && hk_at(h, hoff, full, start) != total) start++;
     order[0] = (int8_t)start;
     int s = full ^ (1 << start), cur = start, n = 1;
     double target = total;
@@ -157,8 +293,8 @@ __device__ inline void held_karp_order(int k, const double* E, const double* h, 
         while (rem) {
             int u = __ffs(rem) - 1;
             rem &= rem - 1;
-            double hv = hk_value(h, s, u);
-            if (E[cur * kHS + u] + hv == target) {
+            double hv = hk_at(h, hoff, s, u);
+            if (E[cur * kES + u] + hv == target) {
                 order[n++] = (int8_t)u;
                 target = hv;
                 cur = u;

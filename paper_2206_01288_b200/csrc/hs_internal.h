@@ -5,14 +5,24 @@
 
 namespace hs {
 
+// Held-Karp schedule for one k (<= 8): packed state words grouped by layer
+// (see hs_eval.cuh), layer starts, and compact offsets off[s].
+struct HKTables {
+    const uint32_t* states;
+    int nstates;
+    int lay[18];
+    const uint16_t* hoff;
+    int nhoff;
+};
+
 struct EvalArgs {
     int n, k, m;
-    const double* dp;      // n*n data-parallel pair seconds (0 diagonal)
-    const uint32_t* rank;  // n*n rank of PP entries among distinct values
-    const double* vals;    // distinct PP values, ascending
-    const uint16_t* states;
-    int nstates;
-    int off[18];
+    const double* dp;    // n*n data-parallel pair seconds (0 diagonal)
+    const void* rank;    // n*n rank of PP entries among distinct values (u16 or u32)
+    bool key16;          // rank table is uint16
+    int nvals;           // distinct PP values
+    const double* vals;  // distinct PP values, ascending
+    HKTables hk;
     const int16_t* groups;  // [P][k][m], members ascending
     int64_t P;
     double* total;
@@ -24,14 +34,11 @@ struct EvalArgs {
 };
 
 struct EvalPlan {
-    bool smem_tables;
+    bool smem_tables, m8;
     int warps, blocks;
     size_t smem;
 };
 
-struct PathOff {
-    int off[18];
-};
 
 int launch_build_tables(int n, const double* lat, const double* bw, int d_dp, double dp_num, double pp_num,
                         double sw_num, double* dp, double* pp, double* sw, cudaStream_t s);
@@ -39,7 +46,8 @@ int launch_rank(int64_t nn, const double* pp, const double* vals, int nvals, uin
 int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan);
 int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s);
 int launch_bottleneck_batch(const double* w, int m, int64_t B, double* out, cudaStream_t s);
-int launch_path_batch(const double* w, int k, int64_t B, const uint16_t* states, int nstates, const PathOff& po,
-                      double* total, int8_t* order, int sm_count, cudaStream_t s);
+int launch_narrow(int64_t nn, const uint32_t* src, uint16_t* dst, cudaStream_t s);
+int launch_path_batch(const double* w, int k, int64_t B, const HKTables& t, double* total, int8_t* order,
+                      int sm_count, cudaStream_t s);
 
 }  // namespace hs

@@ -62,35 +62,54 @@ struct WarpLayout {
     int h_off, e_off, pg_off, mem_off, seen_off, bytes;
 };
 
-template <bool kSmemTables>
+// Per-CTA copy of the Held-Karp state list and compact offsets.
+struct HKSmem {
+    const uint32_t* states;
+    const int* lay;
+    const uint16_t* hoff;
+};
+
+__device__ __forceinline__ size_t hk_smem_bytes(const HKTables& t) {
+    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
+}
+
+__device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* base) {
+    uint32_t* st = reinterpret_cast<uint32_t*>(base);
+    size_t off = ((size_t)t.nstates * 4 + 15) & ~(size_t)15;
+    int* lay = reinterpret_cast<int*>(base + off);
+    off += 80;
+    uint16_t* hoff = reinterpret_cast<uint16_t*>(base + off);
+    for (int i = threadIdx.x; i < t.nstates; i += blockDim.x) st[i] = t.states[i];
+    for (int i = threadIdx.x; i < t.nhoff; i += blockDim.x) hoff[i] = t.hoff[i];
+    if (threadIdx.x < 18) lay[threadIdx.x] = t.lay[threadIdx.x];
+    return HKSmem{st, lay, hoff};
+}
+
+template <bool kSmemTables, typename KeyT, bool kM8>
 __global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, WarpLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const int n = a.n, k = a.k, m = a.m, km = k * m;
-    size_t off = 0;
-    uint16_t* st = reinterpret_cast<uint16_t*>(smem);
-    off += (size_t)((a.nstates * 2 + 15) & ~15);
-    int* soff = reinterpret_cast<int*>(smem + off);
-    off += 96;
+    const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m;
+    HKSmem hk = hk_stage(a.hk, smem);
+    size_t off = hk_smem_bytes(a.hk);
     const double* DP;
-    const uint32_t* RK;
+    const KeyT* RK;
     if (kSmemTables) {
         double* sdp = reinterpret_cast<double*>(smem + off);
         off += (size_t)n * n * 8;
-        uint32_t* srk = reinterpret_cast<uint32_t*>(smem + off);
-        off += ((size_t)n * n * 4 + 15) & ~(size_t)15;
+        KeyT* srk = reinterpret_cast<KeyT*>(smem + off);
+        off += ((size_t)n * n * sizeof(KeyT) + 15) & ~(size_t)15;
+        const KeyT* grk = reinterpret_cast<const KeyT*>(a.rank);
         for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
             sdp[i] = a.dp[i];
-            srk[i] = a.rank[i];
+            srk[i] = grk[i];
         }
         DP = sdp;
         RK = srk;
     } else {
         DP = a.dp;
-        RK = a.rank;
+        RK = reinterpret_cast<const KeyT*>(a.rank);
     }
-    for (int i = threadIdx.x; i < a.nstates; i += blockDim.x) st[i] = a.states[i];
-    if (threadIdx.x < 18) soff[threadIdx.x] = a.off[threadIdx.x];
     unsigned char* wbase = smem + off + (size_t)wid * wl.bytes;
     double* h = reinterpret_cast<double*>(wbase + wl.h_off);
     double* E = reinterpret_cast<double*>(wbase + wl.e_off);
@@ -156,22 +175,37 @@ __global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, WarpLayout w
             decode_pair(t, k, j, j2);
             const int16_t* A = mem + j * m;
             const int16_t* B = mem + j2 * m;
-            uint32_t L = bottleneck_threshold<uint32_t>(
-                m, [&](int r, int c) { return RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
+            uint32_t L;
+            if (kM8) {
+                int b[8];
+#pragma unroll
+                for (int c = 0; c < 8; c++) b[c] = B[c];
+                uint32_t K[8][4];
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const KeyT* row = RK + (size_t)A[r] * n;
+#pragma unroll
+                    for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
+                }
+                L = Match8::solve(K);
+            } else {
+                L = bottleneck_threshold<uint32_t>(
+                    m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
+            }
             double v = a.vals[L];
-            E[j * kHS + j2] = v;
-            E[j2 * kHS + j] = v;
+            E[j * kES + j2] = v;
+            E[j2 * kES + j] = v;
         }
-        if (lane < k) E[lane * kHS + lane] = 0.0;
+        if (lane < k) E[lane * kES + lane] = 0.0;
         __syncwarp();
-        double pipe = warp_held_karp(k, E, h, st, soff, lane);
+        double pipe = warp_held_karp(k, E, h, hk.states, hk.lay, lane);
         double datap = pg[0];
         for (int g = 1; g < k; g++) datap = dmax(datap, pg[g]);
         if (lane == 0) {
             a.total[p] = datap + pipe;
             if (a.datap) a.datap[p] = datap;
             if (a.pipe) a.pipe[p] = pipe;
-            if (a.order) held_karp_order(k, E, h, pipe, a.order + p * k);
+            if (a.order) held_karp_order(k, E, h, hk.hoff, pipe, a.order + p * k);
         }
         if (a.per_group && lane < k) a.per_group[p * k + lane] = pg[lane];
         __syncwarp();
@@ -188,28 +222,24 @@ __global__ void bottleneck_batch_kernel(const double* __restrict__ w, int m, int
     }
 }
 
-__global__ void path_batch_kernel(const double* __restrict__ w, int k, int64_t B, const uint16_t* __restrict__ states,
-                                  int nstates, PathOff po, double* __restrict__ total, int8_t* __restrict__ order) {
+__global__ void path_batch_kernel(const double* __restrict__ w, int k, int64_t B, HKTables t,
+                                  double* __restrict__ total, int8_t* __restrict__ order) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    uint16_t* st = reinterpret_cast<uint16_t*>(smem);
-    size_t off = (size_t)((nstates * 2 + 15) & ~15);
-    int* soff = reinterpret_cast<int*>(smem + off);
-    off += 96;
-    const int hsz = (1 << k) * kHS;
-    double* h = reinterpret_cast<double*>(smem + off) + (size_t)wid * (hsz + kHS * kHS);
-    double* E = h + hsz;
-    for (int i = threadIdx.x; i < nstates; i += blockDim.x) st[i] = states[i];
-    if (threadIdx.x < 18) soff[threadIdx.x] = po.off[threadIdx.x];
+    HKSmem hk = hk_stage(t, smem);
+    size_t off = hk_smem_bytes(t);
+    const int hsz = (k << (k - 1)) + 8 * kES;
+    double* h = reinterpret_cast<double*>(smem + off) + (size_t)wid * hsz;
+    double* E = h + (k << (k - 1));
     __syncthreads();
     for (int64_t b = (int64_t)blockIdx.x * W + wid; b < B; b += (int64_t)gridDim.x * W) {
         const double* src = w + b * k * k;
-        for (int i = lane; i < k * k; i += kWarp) E[(i / k) * kHS + (i % k)] = src[i];
+        for (int i = lane; i < k * k; i += kWarp) E[(i / k) * kES + (i % k)] = src[i];
         __syncwarp();
-        double t = warp_held_karp(k, E, h, st, soff, lane);
+        double tt = warp_held_karp(k, E, h, hk.states, hk.lay, lane);
         if (lane == 0) {
-            total[b] = t;
-            if (order) held_karp_order(k, E, h, t, order + b * k);
+            total[b] = tt;
+            if (order) held_karp_order(k, E, h, hk.hoff, tt, order + b * k);
         }
         __syncwarp();
     }
@@ -221,20 +251,24 @@ __global__ void path_batch_kernel(const double* __restrict__ w, int k, int64_t B
 static WarpLayout warp_layout(int k, int m) {
     WarpLayout wl;
     int km = k * m;
-    int hsz = std::max((1 << k) * kHS, km);
+    int hsz = std::max(k << (k - 1), km);
     int o = 0;
     wl.h_off = o;
     o += hsz * 8;
     wl.e_off = o;
-    o += kHS * kHS * 8;
+    o += 8 * kES * 8;
     wl.pg_off = o;
-    o += kHS * 8;
+    o += 8 * 8;
     wl.mem_off = o;
     o += (km * 2 + 15) & ~15;
     wl.seen_off = o;
     o += 32 * 4;
     wl.bytes = (o + 15) & ~15;
     return wl;
+}
+
+static size_t hk_bytes_host(const HKTables& t) {
+    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
 }
 
 int launch_build_tables(int n, const double* lat, const double* bw, int d_dp, double dp_num, double pp_num,
@@ -251,10 +285,22 @@ int launch_rank(int64_t nn, const double* pp, const double* vals, int nvals, uin
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+__global__ void narrow_kernel(int64_t nn, const uint32_t* __restrict__ src, uint16_t* __restrict__ dst) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nn; x += (int64_t)gridDim.x * blockDim.x)
+        dst[x] = (uint16_t)src[x];
+}
+
+int launch_narrow(int64_t nn, const uint32_t* src, uint16_t* dst, cudaStream_t s) {
+    int blocks = (int)std::min<int64_t>((nn + 255) / 256, 4096);
+    narrow_kernel<<<blocks, 256, 0, s>>>(nn, src, dst);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan) {
     WarpLayout wl = warp_layout(a.k, a.m);
-    size_t fixed = (size_t)((a.nstates * 2 + 15) & ~15) + 96;
-    size_t tables = (size_t)a.n * a.n * 8 + (((size_t)a.n * a.n * 4 + 15) & ~(size_t)15);
+    size_t fixed = hk_bytes_host(a.hk);
+    size_t keyb = a.key16 ? 2 : 4;
+    size_t tables = (size_t)a.n * a.n * 8 + (((size_t)a.n * a.n * keyb + 15) & ~(size_t)15);
     bool smem_tables = fixed + tables + 4 * (size_t)wl.bytes <= smem_optin;
     size_t base = fixed + (smem_tables ? tables : 0);
     if (base + wl.bytes > smem_optin) return -2;
@@ -263,20 +309,35 @@ int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan
     plan->warps = W;
     plan->smem = base + (size_t)W * wl.bytes;
     plan->blocks = sm_count;
+    plan->m8 = a.key16 && a.m == 8 && a.nvals <= 0x8000;
     return 0;
+}
+
+template <bool S, typename KT, bool M8>
+static void launch_one(const EvalArgs& a, const EvalPlan& plan, const WarpLayout& wl, int blocks, cudaStream_t s) {
+    cudaFuncSetAttribute(eval_warp_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    eval_warp_kernel<S, KT, M8><<<blocks, plan.warps * 32, plan.smem, s>>>(a, wl);
 }
 
 int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s) {
     if (a.P == 0) return 0;
     WarpLayout wl = warp_layout(a.k, a.m);
-    int64_t warps_needed = a.P;
-    int blocks = (int)std::min<int64_t>(plan.blocks, (warps_needed + plan.warps - 1) / plan.warps);
-    if (plan.smem_tables) {
-        cudaFuncSetAttribute(eval_warp_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-        eval_warp_kernel<true><<<blocks, plan.warps * 32, plan.smem, s>>>(a, wl);
+    int blocks = (int)std::min<int64_t>(plan.blocks, (a.P + plan.warps - 1) / plan.warps);
+    if (plan.m8) {
+        if (plan.smem_tables)
+            launch_one<true, uint16_t, true>(a, plan, wl, blocks, s);
+        else
+            launch_one<false, uint16_t, true>(a, plan, wl, blocks, s);
+    } else if (a.key16) {
+        if (plan.smem_tables)
+            launch_one<true, uint16_t, false>(a, plan, wl, blocks, s);
+        else
+            launch_one<false, uint16_t, false>(a, plan, wl, blocks, s);
     } else {
-        cudaFuncSetAttribute(eval_warp_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-        eval_warp_kernel<false><<<blocks, plan.warps * 32, plan.smem, s>>>(a, wl);
+        if (plan.smem_tables)
+            launch_one<true, uint32_t, false>(a, plan, wl, blocks, s);
+        else
+            launch_one<false, uint32_t, false>(a, plan, wl, blocks, s);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -288,14 +349,14 @@ int launch_bottleneck_batch(const double* w, int m, int64_t B, double* out, cuda
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int launch_path_batch(const double* w, int k, int64_t B, const uint16_t* states, int nstates, const PathOff& po,
-                      double* total, int8_t* order, int sm_count, cudaStream_t s) {
+int launch_path_batch(const double* w, int k, int64_t B, const HKTables& t, double* total, int8_t* order,
+                      int sm_count, cudaStream_t s) {
     if (B == 0) return 0;
     int W = 4;
-    size_t smem = (size_t)((nstates * 2 + 15) & ~15) + 96 + (size_t)W * ((1 << k) * kHS + kHS * kHS) * 8;
+    size_t smem = hk_bytes_host(t) + (size_t)W * ((k << (k - 1)) + 8 * kES) * 8;
     cudaFuncSetAttribute(path_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int blocks = (int)std::min<int64_t>((B + W - 1) / W, (int64_t)sm_count * 8);
-    path_batch_kernel<<<blocks, W * 32, smem, s>>>(w, k, B, states, nstates, po, total, order);
+    path_batch_kernel<<<blocks, W * 32, smem, s>>>(w, k, B, t, total, order);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
