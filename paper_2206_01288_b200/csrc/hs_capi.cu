@@ -48,14 +48,16 @@ void hk_schedule(int k, std::vector<uint32_t>& st, std::vector<uint16_t>& hoff, 
         if (__builtin_popcount(s) >= 2) acc += __builtin_popcount(s);
     }
     for (int i = 0; i < 18; i++) lay[i] = 0;
+    // r-major within a layer: the k-|r| states sharing r = s \ u sit on
+    // adjacent lanes and read the same h[r][.] row (smem broadcast).
     for (int p = 0; p < 18; p++) {
         lay[p] = (int)st.size();
         if (p < 2 || p > k) continue;
-        for (int s = 0; s < (1 << k); s++) {
-            if (__builtin_popcount(s) != p) continue;
+        for (int r = 0; r < (1 << k); r++) {
+            if (__builtin_popcount(r) != p - 1) continue;
             for (int u = 0; u < k; u++) {
-                if (!(s >> u & 1)) continue;
-                int r = s ^ (1 << u);
+                if (r >> u & 1) continue;
+                int s = r | (1 << u);
                 uint32_t dst = hoff[s] + __builtin_popcount(s & ((1 << u) - 1));
                 uint32_t offr = __builtin_popcount(r) >= 2 ? hoff[r] : 0;
                 st.push_back(offr | (dst << 10) | ((uint32_t)u << 20) | ((uint32_t)r << 23));

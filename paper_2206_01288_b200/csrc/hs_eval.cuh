@@ -242,8 +242,11 @@ __device__ inline double warp_held_karp(int k, const double* E, double* h, const
                                         int lane) {
     if (k == 1) return 0.0;
     for (int p = 2; p <= k; p++) {
-        for (int idx = lay[p] + lane; idx < lay[p + 1]; idx += kWarp) {
-            uint32_t w = states[idx];
+        const int end = lay[p + 1];
+        uint32_t wn = lay[p] + lane < end ? states[lay[p] + lane] : 0u;
+        for (int idx = lay[p] + lane; idx < end; idx += kWarp) {
+            uint32_t w = wn;
+            if (idx + kWarp < end) wn = states[idx + kWarp];  // prefetch the next state word
             uint32_t r = w >> 23;
             int u = (w >> 20) & 7;
             const double* Eu = E + u * kES;
