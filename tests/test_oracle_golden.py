@@ -203,3 +203,9 @@ def test_oracle_assignments():
         assert grid.tolist() == c["grid"] and list(order) == c["order"]
         o3, _ = O.Oracle.of(g, w).evaluate_assignment(grid)
         assert o3[0] == fx(c["total"])
+
+
+@pytest.mark.parametrize("idx", range(len(I.fixture("evolve_1000.json")["runs"])))
+def test_oracle_evolve_1000_generations(idx):
+    """The GA time-to-converge anchors (pop 64, 1000 gens, ours, seed 0)."""
+    _check_run(I.fixture("evolve_1000.json")["runs"][idx])
