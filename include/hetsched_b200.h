@@ -74,6 +74,62 @@ int hs_bottleneck_batch(const double *w, int m, int64_t B, double *out, int devi
  * optimal order [B][k] (order may be NULL).  Device pointers. */
 int hs_path_batch(const double *w, int k, int64_t B, double *total, int8_t *order, int device, void *stream);
 
+
+/* ---------------- search: K2 (swap gains / local search), K3 (GA) ----------
+ * All search entry points reproduce numpy's PCG64 stream draw for draw: the
+ * caller passes bit_generator.state and receives the advanced state back
+ * (so later caller draws stay aligned, scheduler.py:490-512). */
+
+typedef struct {
+    int32_t pop_size, generations, kind /* 0 ours, 1 kl, 2 none */, max_passes, patience /* <= 0: none */;
+} hs_ga_config;
+
+typedef struct hs_ga hs_ga;
+
+/* A GA session of `islands` independent steady-state GAs, one CTA each, with
+ * island i seeded by rng[i] (evolve, scheduler.py:515-574; the numpy
+ * Generator(PCG64(seed)) state of :528).  Population and RNG stay on the
+ * device between hs_ga_run calls, so a run can be cut into epochs. */
+int hs_ga_create(hs_instance *h, const hs_ga_config *cfg, int islands, const hs_pcg64 *rng, hs_ga **out);
+/* advance every island to generation `until` (or its patience stop) */
+int hs_ga_run(hs_ga *ga, int until, void *stream);
+/* island migration (no reference counterpart): export each
+ * island's `elites` best members (cost, then index) as int16 [islands][E][k*m]
+ * + float64 [islands][E] device buffers; import replaces the island's worst
+ * members (first maximum, one per migrant, only if the migrant is strictly
+ * cheaper) with migrants[src[i]] for island i. */
+int hs_ga_export(hs_ga *ga, int elites, int16_t *groups, double *costs, void *stream);
+int hs_ga_import(hs_ga *ga, int elites, const int16_t *groups, const double *costs, const int32_t *src, void *stream);
+/* finalize (canonical best, priced once more, :570-574) and copy results to
+ * host buffers: best_groups [islands][k*m], best3 [islands][3] (total, datap,
+ * pipelinep), best_per_group [islands][k], best_order [islands][k],
+ * trace_best / trace_mean [islands][generations], trace_len [islands],
+ * evaluations [islands], rng [islands] (advanced states).  NULL skips. */
+int hs_ga_result(hs_ga *ga, int16_t *best_groups, double *best3, double *best_per_group, int8_t *best_order,
+                 double *trace_best, double *trace_mean, int32_t *trace_len, int64_t *evaluations, hs_pcg64 *rng);
+int hs_ga_destroy(hs_ga *ga);
+
+/* local_search (scheduler.py:490-512, _refine :455-487) on B partitions,
+ * each with its own stream; host buffers. */
+int hs_local_search(hs_instance *h, int kind, int max_passes, int B, const int16_t *groups, hs_pcg64 *rng,
+                    int16_t *out, double *out_total, int32_t *evaluations);
+/* one refinement pass (_pass_ours phase / _pass_kl, scheduler.py:394-449) */
+int hs_refine_pass(hs_instance *h, int kind, int phase, int B, const int16_t *groups, hs_pcg64 *rng, int16_t *out,
+                   int32_t *changed);
+/* crossover (scheduler.py:139-174) on B parent pairs of shape d_pp x d_dp
+ * (n = d_pp*d_dp), one stream each; host buffers */
+int hs_crossover(int n, int d_pp, int d_dp, int device, int B, const int16_t *p1, const int16_t *p2, hs_pcg64 *rng,
+                 int16_t *out);
+/* gain_ours (kind 0, q = j, j2, d1, d2, d1', d2') / gain_kl (kind 1, q = d, d2,
+ * group(d), group(d2)), scheduler.py:181-230, on any n x n surrogate table
+ * sw (SurrogateWeights.w); host buffers, q is int32 [B][6] */
+int hs_gains(int n, int d_pp, int d_dp, int device, const double *sw, int kind, int B, const int16_t *groups,
+             const int32_t *q, double *out);
+/* init_population / random_partition (scheduler.py:114-136): B sequential
+ * random_partition draws from one stream into int16 [B][n] (groups of d_dp,
+ * members ascending) */
+int hs_random_partitions(int n, int d_pp, int d_dp, int device, int B, hs_pcg64 *rng, int16_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,11 @@ class PCG64(C.Structure):
         rng.bit_generator.state = st
 
 
+class GAConfig(C.Structure):
+    _fields_ = [("pop_size", C.c_int32), ("generations", C.c_int32), ("kind", C.c_int32),
+                ("max_passes", C.c_int32), ("patience", C.c_int32)]
+
+
 _lock = threading.Lock()
 _lib = None
 
@@ -95,15 +100,29 @@ def lib():
         L.hs_eval_batch_host.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
         L.hs_bottleneck_batch.argtypes = [vp, i32, i64, vp, i32, vp]
         L.hs_path_batch.argtypes = [vp, i32, i64, vp, vp, i32, vp]
-        for name in ("hs_instance_create", "hs_instance_destroy", "hs_instance_tables", "hs_eval_batch",
-                     "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch"):
-            getattr(L, name).restype = i32
+        pcg = C.POINTER(PCG64)
+        L.hs_ga_create.argtypes = [vp, C.POINTER(GAConfig), i32, pcg, C.POINTER(vp)]
+        L.hs_ga_run.argtypes = [vp, i32, vp]
+        L.hs_ga_export.argtypes = [vp, i32, vp, vp, vp]
+        L.hs_ga_import.argtypes = [vp, i32, vp, vp, vp, vp]
+        L.hs_ga_result.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, pcg]
+        L.hs_ga_destroy.argtypes = [vp]
+        L.hs_local_search.argtypes = [vp, i32, i32, i32, vp, pcg, vp, vp, vp]
+        L.hs_refine_pass.argtypes = [vp, i32, i32, i32, vp, pcg, vp, vp]
+        L.hs_crossover.argtypes = [i32, i32, i32, i32, i32, vp, vp, pcg, vp]
+        L.hs_gains.argtypes = [i32, i32, i32, i32, vp, i32, i32, vp, vp, vp]
+        L.hs_random_partitions.argtypes = [i32, i32, i32, i32, i32, pcg, vp]
+        for name in EXPORTS:
+            if name not in ("hs_version", "hs_last_error"):
+                getattr(L, name).restype = i32
         _lib = L
         return L
 
 
 EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_destroy", "hs_instance_tables",
-           "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch")
+           "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_run",
+           "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
+           "hs_crossover", "hs_gains", "hs_random_partitions")
 
 
 def check(rc: int, what: str) -> None:

@@ -13,13 +13,13 @@
 
 #include "../../include/hetsched_b200.h"
 #include "hs_eval.cuh"
-#include "hs_internal.h"
+#include "hs_instance.h"
 
-namespace {
+namespace hsx {
 
 thread_local std::string g_err;
 
-int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
+int fail(int code, const char* what, cudaError_t e) {
     char buf[512];
     if (e != cudaSuccess)
         snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
@@ -29,11 +29,6 @@ int fail(int code, const char* what, cudaError_t e = cudaSuccess) {
     return code;
 }
 
-#define CK(call, what)                               \
-    do {                                             \
-        cudaError_t e_ = (call);                     \
-        if (e_ != cudaSuccess) return fail(-1, what, e_); \
-    } while (0)
 
 // Held-Karp schedule for k <= 8 (see hs_eval.cuh, warp_held_karp): compact
 // offsets off[s] (entries for |s| >= 2, s ascending), and per state (s, u)
@@ -98,39 +93,12 @@ int get_hk(int device, int k, hs::HKTables* out) {
     return 0;
 }
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
+}  // namespace hsx
 
-}  // namespace
-
-struct hs_instance {
-    int device = 0, n = 0, k = 0, m = 0, sm_count = 0;
-    size_t smem_optin = 0;
-    double *lat = nullptr, *bw = nullptr, *dp = nullptr, *pp = nullptr, *sw = nullptr, *vals = nullptr;
-    uint32_t* rank = nullptr;
-    uint16_t* rank16 = nullptr;
-    int nvals = 0;
-    hs::HKTables hk{};
-    int* invalid = nullptr;
-    hs::EvalPlan plan{};
-    // host-buffer path
-    std::mutex mu;
-    int64_t chunk = 0;
-    int16_t* cg[2] = {nullptr, nullptr};
-    double* co[2] = {nullptr, nullptr};
-    int* cinv = nullptr;
-    cudaStream_t cs[2] = {nullptr, nullptr};
-};
+using hsx::fail;
+using hsx::get_hk;
+using hsx::DeviceGuard;
+using hsx::g_err;
 
 static hs::EvalArgs base_args(const hs_instance* h) {
     hs::EvalArgs a{};
@@ -168,6 +136,11 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     h->sm_count = prop.multiProcessorCount;
+    // the search kernels' call chains (GA driver -> crossover / passes ->
+    // warp evaluator) need more than the default 1 KiB per-thread stack
+    size_t stack = 0;
+    CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "cudaDeviceGetLimit");
+    if (stack < 8192) CK(cudaDeviceSetLimit(cudaLimitStackSize, 8192), "cudaDeviceSetLimit");
     h->smem_optin = prop.sharedMemPerBlockOptin;
     size_t nn = (size_t)n * n;
     CK(cudaMalloc(&h->lat, nn * 8), "cudaMalloc");

@@ -1,0 +1,54 @@
+// hs_instance.h -- the C-ABI handle and shared host helpers.
+#pragma once
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "../../include/hetsched_b200.h"
+#include "hs_internal.h"
+
+namespace hsx {
+
+int fail(int code, const char* what, cudaError_t e = cudaSuccess);
+int get_hk(int device, int k, hs::HKTables* out);
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+}  // namespace hsx
+
+#define CK(call, what)                                              \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return hsx::fail(-1, what, e_);      \
+    } while (0)
+
+struct hs_instance {
+    int device = 0, n = 0, k = 0, m = 0, sm_count = 0;
+    size_t smem_optin = 0;
+    double *lat = nullptr, *bw = nullptr, *dp = nullptr, *pp = nullptr, *sw = nullptr, *vals = nullptr;
+    uint32_t* rank = nullptr;
+    uint16_t* rank16 = nullptr;
+    int nvals = 0;
+    hs::HKTables hk{};
+    int* invalid = nullptr;
+    hs::EvalPlan plan{};
+    // host-buffer path
+    std::mutex mu;
+    int64_t chunk = 0;
+    int16_t* cg[2] = {nullptr, nullptr};
+    double* co[2] = {nullptr, nullptr};
+    int* cinv = nullptr;
+    cudaStream_t cs[2] = {nullptr, nullptr};
+};
+

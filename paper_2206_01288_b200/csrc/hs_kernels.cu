@@ -13,8 +13,7 @@
 //                            Persistent grid, pair tables staged in smem.
 //   bottleneck_batch / path_batch : the public single-matrix solvers
 //                            (combinatorics.py:128-131,232-251) over a batch.
-#include "hs_eval.cuh"
-#include "hs_internal.h"
+#include "hs_warp_eval.cuh"
 
 #include <algorithm>
 
@@ -49,102 +48,24 @@ __global__ void rank_kernel(int64_t nn, const double* __restrict__ pp, const dou
     }
 }
 
-__device__ __forceinline__ void decode_pair(int t, int k, int& j, int& j2) {
-    j = 0;
-    while (t >= k - 1 - j) {
-        t -= k - 1 - j;
-        j++;
-    }
-    j2 = j + 1 + t;
-}
-
-struct WarpLayout {
-    int h_off, e_off, pg_off, mem_off, seen_off, bytes;
-};
-
-// Per-CTA copy of the Held-Karp state list and compact offsets.
-struct HKSmem {
-    const uint32_t* states;
-    const int* lay;
-    const uint16_t* hoff;
-};
-
-__device__ __forceinline__ size_t hk_smem_bytes(const HKTables& t) {
-    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
-}
-
-__device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* base) {
-    uint32_t* st = reinterpret_cast<uint32_t*>(base);
-    size_t off = ((size_t)t.nstates * 4 + 15) & ~(size_t)15;
-    int* lay = reinterpret_cast<int*>(base + off);
-    off += 80;
-    uint16_t* hoff = reinterpret_cast<uint16_t*>(base + off);
-    for (int i = threadIdx.x; i < t.nstates; i += blockDim.x) st[i] = t.states[i];
-    for (int i = threadIdx.x; i < t.nhoff; i += blockDim.x) hoff[i] = t.hoff[i];
-    if (threadIdx.x < 18) lay[threadIdx.x] = t.lay[threadIdx.x];
-    return HKSmem{st, lay, hoff};
-}
-
 template <bool kSmemTables, typename KeyT, bool kM8>
-__global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, WarpLayout wl) {
+__global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, ScratchLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m;
+    const int k = a.k, m = kM8 ? 8 : a.m, km = k * m;
     HKSmem hk = hk_stage(a.hk, smem);
     size_t off = hk_smem_bytes(a.hk);
-    const double* DP;
-    const KeyT* RK;
-    if (kSmemTables) {
-        double* sdp = reinterpret_cast<double*>(smem + off);
-        off += (size_t)n * n * 8;
-        KeyT* srk = reinterpret_cast<KeyT*>(smem + off);
-        off += ((size_t)n * n * sizeof(KeyT) + 15) & ~(size_t)15;
-        const KeyT* grk = reinterpret_cast<const KeyT*>(a.rank);
-        for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-            sdp[i] = a.dp[i];
-            srk[i] = grk[i];
-        }
-        DP = sdp;
-        RK = srk;
-    } else {
-        DP = a.dp;
-        RK = reinterpret_cast<const KeyT*>(a.rank);
-    }
+    EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(a.n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
     unsigned char* wbase = smem + off + (size_t)wid * wl.bytes;
-    double* h = reinterpret_cast<double*>(wbase + wl.h_off);
-    double* E = reinterpret_cast<double*>(wbase + wl.e_off);
-    double* pg = reinterpret_cast<double*>(wbase + wl.pg_off);
+    WarpScratch ws = scratch_at(wbase, wl);
     int16_t* mem = reinterpret_cast<int16_t*>(wbase + wl.mem_off);
-    uint32_t* seen = reinterpret_cast<uint32_t*>(wbase + wl.seen_off);
     __syncthreads();
 
-    const int nwords = (n + 31) >> 5;
-    const int npairs = k * (k - 1) / 2;
     for (int64_t p = (int64_t)blockIdx.x * W + wid; p < a.P; p += (int64_t)gridDim.x * W) {
         const int16_t* gsrc = a.groups + p * km;
         for (int i = lane; i < km; i += kWarp) mem[i] = gsrc[i];
-        for (int i = lane; i < nwords; i += kWarp) seen[i] = 0;
         __syncwarp();
-        // Partition invariants (costmodel.py:58-72): in range, ascending
-        // within each group, and covering 0..n-1 (k*m == n, so covering
-        // implies disjoint).
-        bool bad = false;
-        for (int i = lane; i < km; i += kWarp) {
-            int d = mem[i];
-            if (d < 0 || d >= n) {
-                bad = true;
-            } else {
-                if (i % m != 0 && mem[i - 1] >= d) bad = true;
-                atomicOr(&seen[d >> 5], 1u << (d & 31));
-            }
-        }
-        __syncwarp();
-        for (int i = lane; i < nwords; i += kWarp) {
-            int bits = min(32, n - i * 32);
-            uint32_t want = bits == 32 ? 0xffffffffu : ((1u << bits) - 1u);
-            if (seen[i] != want) bad = true;
-        }
-        if (__any_sync(0xffffffffu, bad)) {
+        if (!warp_valid(a.n, k, m, mem, ws.seen, lane)) {
             if (lane == 0) {
                 const double nan = __longlong_as_double(0x7ff8000000000000LL);
                 a.total[p] = nan;
@@ -155,65 +76,19 @@ __global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, WarpLayout w
             __syncwarp();
             continue;
         }
-        // data-parallel level (costmodel.py:154-175): per-row numpy pairwise
-        // sum over the sorted members (diagonal 0.0 in its slot), max per group
-        for (int r = lane; r < km; r += kWarp) {
-            int g = r / m;
-            const int16_t* gm = mem + g * m;
-            const double* row = DP + (size_t)gm[r - g * m] * n;
-            h[r] = pairwise_sum(m, [&](int c) { return row[gm[c]]; });
-        }
-        __syncwarp();
-        if (lane < k) {
-            double mx = h[lane * m];
-            for (int i = 1; i < m; i++) mx = dmax(mx, h[lane * m + i]);
-            pg[lane] = mx;
-        }
-        // pipeline edges (costmodel.py:200-208): bottleneck of each group pair
-        for (int t = lane; t < npairs; t += kWarp) {
-            int j, j2;
-            decode_pair(t, k, j, j2);
-            const int16_t* A = mem + j * m;
-            const int16_t* B = mem + j2 * m;
-            uint32_t L;
-            if (kM8) {
-                int b[8];
-#pragma unroll
-                for (int c = 0; c < 8; c++) b[c] = B[c];
-                uint32_t K[8][4];
-#pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const KeyT* row = RK + (size_t)A[r] * n;
-#pragma unroll
-                    for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
-                }
-                L = Match8::solve(K);
-            } else {
-                L = bottleneck_threshold<uint32_t>(
-                    m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
-            }
-            double v = a.vals[L];
-            E[j * kES + j2] = v;
-            E[j2 * kES + j] = v;
-        }
-        if (lane < k) E[lane * kES + lane] = 0.0;
-        __syncwarp();
-        double pipe = warp_held_karp(k, E, h, hk.states, hk.lay, lane);
-        double datap = pg[0];
-        for (int g = 1; g < k; g++) datap = dmax(datap, pg[g]);
+        double datap, pipe;
+        warp_price<KeyT, kM8>(v, ws, mem, lane, datap, pipe);
         if (lane == 0) {
             a.total[p] = datap + pipe;
             if (a.datap) a.datap[p] = datap;
             if (a.pipe) a.pipe[p] = pipe;
-            if (a.order) held_karp_order(k, E, h, hk.hoff, pipe, a.order + p * k);
+            if (a.order) held_karp_order(k, ws.E, ws.h, hk.hoff, pipe, a.order + p * k);
         }
-        if (a.per_group && lane < k) a.per_group[p * k + lane] = pg[lane];
+        if (a.per_group && lane < k) a.per_group[p * k + lane] = ws.pg[lane];
         __syncwarp();
     }
 }
 
-// ---------------------------------------------------------------------------
-// public single-matrix solvers, batched
 
 __global__ void bottleneck_batch_kernel(const double* __restrict__ w, int m, int64_t B, double* __restrict__ out) {
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
@@ -248,28 +123,7 @@ __global__ void path_batch_kernel(const double* __restrict__ w, int k, int64_t B
 // ---------------------------------------------------------------------------
 // launchers
 
-static WarpLayout warp_layout(int k, int m) {
-    WarpLayout wl;
-    int km = k * m;
-    int hsz = std::max(k << (k - 1), km);
-    int o = 0;
-    wl.h_off = o;
-    o += hsz * 8;
-    wl.e_off = o;
-    o += 8 * kES * 8;
-    wl.pg_off = o;
-    o += 8 * 8;
-    wl.mem_off = o;
-    o += (km * 2 + 15) & ~15;
-    wl.seen_off = o;
-    o += 32 * 4;
-    wl.bytes = (o + 15) & ~15;
-    return wl;
-}
-
-static size_t hk_bytes_host(const HKTables& t) {
-    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
-}
+static size_t hk_bytes_host(const HKTables& t) { return hk_smem_bytes(t); }
 
 int launch_build_tables(int n, const double* lat, const double* bw, int d_dp, double dp_num, double pp_num,
                         double sw_num, double* dp, double* pp, double* sw, cudaStream_t s) {
@@ -297,7 +151,7 @@ int launch_narrow(int64_t nn, const uint32_t* src, uint16_t* dst, cudaStream_t s
 }
 
 int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan) {
-    WarpLayout wl = warp_layout(a.k, a.m);
+    ScratchLayout wl = scratch_layout(a.k, a.m);
     size_t fixed = hk_bytes_host(a.hk);
     size_t keyb = a.key16 ? 2 : 4;
     size_t tables = (size_t)a.n * a.n * 8 + (((size_t)a.n * a.n * keyb + 15) & ~(size_t)15);
@@ -314,14 +168,14 @@ int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan
 }
 
 template <bool S, typename KT, bool M8>
-static void launch_one(const EvalArgs& a, const EvalPlan& plan, const WarpLayout& wl, int blocks, cudaStream_t s) {
+static void launch_one(const EvalArgs& a, const EvalPlan& plan, const ScratchLayout& wl, int blocks, cudaStream_t s) {
     cudaFuncSetAttribute(eval_warp_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
     eval_warp_kernel<S, KT, M8><<<blocks, plan.warps * 32, plan.smem, s>>>(a, wl);
 }
 
 int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s) {
     if (a.P == 0) return 0;
-    WarpLayout wl = warp_layout(a.k, a.m);
+    ScratchLayout wl = scratch_layout(a.k, a.m);
     int blocks = (int)std::min<int64_t>(plan.blocks, (a.P + plan.warps - 1) / plan.warps);
     if (plan.m8) {
         if (plan.smem_tables)

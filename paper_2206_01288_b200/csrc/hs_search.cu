@@ -1,0 +1,1207 @@
+// hs_search.cu -- K2 (surrogate swap gains / local search) and K3 (the GA
+// generation loop) on sm_100a, bit-for-bit with hetsched/scheduler.py.
+//
+// One CTA runs one GA instance (an island).  Warp 0 is the driver: it owns
+// the numpy PCG64 stream (lane 0) and executes crossover (scheduler.py:139-174)
+// and the refinement passes (_pass_ours :394-428 with _best_candidate :260-276
+// and _chain_round :299-391; _pass_kl :431-449) with its 32 lanes sharing the
+// data-parallel parts (fast edge, pairwise sums, group means, home costs, KL
+// gain matrices).  The passes never read true costs (H4), so a
+// generation is: driver produces the offspring plus <= max_passes snapshots ->
+// every warp prices snapshots with the K1 warp evaluator -> driver applies
+// _refine's first-strict-minimum rule and evolve's replacement / trace rules
+// (:548-569).  Population, costs, best and RNG live in global memory between
+// launches, so a run can be cut into epochs (island migration).
+#include <cfloat>
+#include <climits>
+
+#include "hs_rng.cuh"
+#include "hs_search.h"
+#include "hs_warp_eval.cuh"
+
+namespace hs {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ void warp_argmin(double& v, int& i) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double v2 = __shfl_xor_sync(kFull, v, o);
+        int i2 = __shfl_xor_sync(kFull, i, o);
+        if (v2 < v || (v2 == v && i2 < i)) {
+            v = v2;
+            i = i2;
+        }
+    }
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        double v2 = __shfl_xor_sync(kFull, v, o);
+        int i2 = __shfl_xor_sync(kFull, i, o);
+        if (v2 > v || (v2 == v && i2 < i)) {
+            v = v2;
+            i = i2;
+        }
+    }
+}
+
+// numpy pairwise sum of an array (any n; recursion only beyond 128)
+__device__ double pw_array(const double* a, int n) {
+    if (n <= 128) return pairwise_sum(n, [&](int i) { return a[i]; });
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return pw_array(a, n2) + pw_array(a + n2, n - n2);
+}
+
+// ---------------------------------------------------------------------------
+// driver-warp working state (shared memory)
+
+struct LS {
+    int n, k, m, cap;
+    const double* W;  // surrogate weights n x n (scheduler.py:84-88)
+    int16_t* G;       // k x cap members, ascending
+    int* sz;          // k sizes
+    double* mean;     // n x k: mean[u*k+i] = seq_sum(W[u, G_i]) / sz_i
+    double* home;     // n: cheapest intra-group link of each device
+    int* valid;       // [0]: mean columns valid (bitmask), [1]: home groups valid
+    uint32_t* locked;  // n-bit set
+    int* nlocked;
+    int16_t* perm;    // C(k,2)
+    double* f64;      // scratch: 4*cap (KL sums) and chain steps/closers
+    int* i32;         // scratch: chain moves (3*k), misc
+    int8_t* grp_of;   // n
+};
+
+__device__ __forceinline__ void g_remove(LS& s, int j, int d) {
+    int16_t* g = s.G + j * s.cap;
+    int c = s.sz[j], i = 0;
+    while (i < c && g[i] != d) i++;
+    for (; i + 1 < c; i++) g[i] = g[i + 1];
+    s.sz[j] = c - 1;
+}
+
+__device__ __forceinline__ void g_insort(LS& s, int j, int d) {  // bisect.insort
+    int16_t* g = s.G + j * s.cap;
+    int i = s.sz[j];
+    while (i > 0 && g[i - 1] > d) {
+        g[i] = g[i - 1];
+        i--;
+    }
+    g[i] = (int16_t)d;
+    s.sz[j]++;
+}
+
+__device__ __forceinline__ double row_pw(const LS& s, int u, const int16_t* grp, int cnt) {
+    const double* wr = s.W + (size_t)u * s.n;
+    if (cnt < 8) {
+        double r = 0.0;
+        for (int i = 0; i < cnt; i++) r += wr[grp[i]];
+        return r;
+    }
+    return pairwise_sum(cnt, [&](int i) { return wr[grp[i]]; });
+}
+
+__device__ __forceinline__ double row_seq_mean(const LS& s, int u, const int16_t* grp, int cnt) {
+    const double* wr = s.W + (size_t)u * s.n;
+    double r = 0.0;
+    for (int i = 0; i < cnt; i++) r += wr[grp[i]];
+    return r / (double)cnt;
+}
+
+// _fast_edge (:237-249): lexicographically first minimum intra-group pair
+__device__ inline void fast_edge(const LS& s, int j, int lane, int& a, int& b) {
+    const int16_t* g = s.G + j * s.cap;
+    int c = s.sz[j];
+    double bv = kInf;
+    int code = INT_MAX;
+    for (int i = lane; i < c; i += kWarp) {
+        const double* wr = s.W + (size_t)g[i] * s.n;
+        for (int l = i + 1; l < c; l++) {
+            double v = wr[g[l]];
+            if (v < bv) {
+                bv = v;
+                code = i * 256 + l;
+            }
+        }
+    }
+    warp_argmin(bv, code);
+    if (code == INT_MAX) code = 1;  // (grp[0], grp[1]) default
+    a = g[code >> 8];
+    b = g[code & 255];
+}
+
+// _best_candidate (:260-276) with _gain_ours (:206-209): the four candidates
+// need only four row sums, computed by lanes 0..3.
+__device__ inline double best_candidate(const LS& s, int j, int j2, int lane, int& oa, int& ob) {
+    int d1, d2, d1p, d2p;
+    fast_edge(s, j, lane, d1, d2);
+    fast_edge(s, j2, lane, d1p, d2p);
+    const int16_t* gj = s.G + j * s.cap;
+    const int16_t* gj2 = s.G + j2 * s.cap;
+    int cj = s.sz[j], cj2 = s.sz[j2];
+    double sum = 0.0;
+    if (lane < 4) {
+        int u = lane == 0 ? d1 : lane == 1 ? d2 : lane == 2 ? d1p : d2p;
+        sum = lane < 2 ? row_pw(s, u, gj2, cj2) : row_pw(s, u, gj, cj);
+    }
+    double S0 = __shfl_sync(kFull, sum, 0), S1 = __shfl_sync(kFull, sum, 1);
+    double S2 = __shfl_sync(kFull, sum, 2), S3 = __shfl_sync(kFull, sum, 3);
+    const int n = s.n;
+    double t1a = S0 / (double)cj2 - s.W[(size_t)d1 * n + d2];   // a = d1, pa = d2
+    double t1b = S1 / (double)cj2 - s.W[(size_t)d2 * n + d1];   // a = d2, pa = d1
+    double t2a = S2 / (double)cj - s.W[(size_t)d1p * n + d2p];  // b = d1p, pb = d2p
+    double t2b = S3 / (double)cj - s.W[(size_t)d2p * n + d1p];  // b = d2p, pb = d1p
+    double g[4] = {t1a + t2a, t1a + t2b, t1b + t2a, t1b + t2b};
+    int A[4] = {d1, d1, d2, d2}, Bv[4] = {d1p, d2p, d1p, d2p};
+    double best = -kInf;
+    oa = d1;
+    ob = d1p;
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+        if (g[c] > best) {
+            best = g[c];
+            oa = A[c];
+            ob = Bv[c];
+        }
+    return best;
+}
+
+__device__ __forceinline__ void invalidate(LS& s, int j) {
+    s.valid[0] &= ~(1 << j);
+    s.valid[1] &= ~(1 << j);
+}
+
+// even phase of _pass_ours: swap sweep over rng.permutation(C(k,2)) pairs
+__device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
+    const int k = s.k, np = k * (k - 1) / 2, d_dp = s.sz[0];
+    if (lane == 0) {
+        for (int i = 0; i < np; i++) s.perm[i] = (int16_t)i;
+        for (int i = np - 1; i >= 1; i--) {
+            int jx = (int)rng.interval((uint64_t)i);
+            int16_t t = s.perm[i];
+            s.perm[i] = s.perm[jx];
+            s.perm[jx] = t;
+        }
+    }
+    __syncwarp();
+    bool changed = false;
+    for (int q = 0; q < np; q++) {
+        int j, j2;
+        decode_pair(s.perm[q], k, j, j2);
+        for (int it = 0; it < d_dp; it++) {
+            int a, b;
+            double gain = best_candidate(s, j, j2, lane, a, b);
+            if (gain <= 0.0) break;
+            if (lane == 0) {  // _swap (:252-257)
+                g_remove(s, j, a);
+                g_remove(s, j2, b);
+                g_insort(s, j2, a);
+                g_insort(s, j, b);
+                invalidate(s, j);
+                invalidate(s, j2);
+            }
+            __syncwarp();
+            changed = true;
+        }
+    }
+    return changed;
+}
+
+__device__ inline void ensure_caches(LS& s, int lane) {
+    const int k = s.k, n = s.n;
+    int mv = s.valid[0], hv = s.valid[1];
+    for (int i = 0; i < k; i++) {
+        const int16_t* g = s.G + i * s.cap;
+        int c = s.sz[i];
+        if (!(mv >> i & 1))
+            for (int u = lane; u < n; u += kWarp) s.mean[u * k + i] = row_seq_mean(s, u, g, c);
+        if (!(hv >> i & 1))
+            for (int a = lane; a < c; a += kWarp) {  // _home_costs (:287-291)
+                const double* wr = s.W + (size_t)g[a] * n;
+                double h = kInf;
+                for (int b = 0; b < c; b++)
+                    if (b != a) h = dmin(h, wr[g[b]]);
+                s.home[g[a]] = h;
+            }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        s.valid[0] = (1 << k) - 1;
+        s.valid[1] = (1 << k) - 1;
+    }
+    __syncwarp();
+}
+
+// fastest_free (:318-328): min by (home, id) over unlocked members; -1 if none
+__device__ __forceinline__ int fastest_free(const LS& s, int i, double& home) {
+    const int16_t* g = s.G + i * s.cap;
+    int c = s.sz[i];
+    if (c < 2) return -1;
+    int best = -1;
+    double bh = 0.0;
+    for (int a = 0; a < c; a++) {
+        int d = g[a];
+        if (s.locked[d >> 5] >> (d & 31) & 1) continue;
+        double h = s.home[d];
+        if (best < 0 || h < bh) {
+            best = d;
+            bh = h;
+        }
+    }
+    home = bh;
+    return best;
+}
+
+// _chain_round (:299-391)
+__device__ __noinline__ bool chain_round(LS& s, int lane) {
+    const int k = s.k, n = s.n;
+    ensure_caches(s, lane);
+    // start group: largest relocation gain, first on ties
+    double gain = -kInf;
+    int idx = INT_MAX;
+    if (lane < k) {
+        double home;
+        int v = fastest_free(s, lane, home);
+        if (v >= 0) {
+            double mx = -kInf;
+            bool first = true;
+            for (int j = 0; j < k; j++) {
+                if (j == lane) continue;
+                double x = s.mean[v * k + j];
+                if (first || x > mx) mx = x;
+                first = false;
+            }
+            gain = mx - home;
+            idx = lane;
+        }
+    }
+    warp_argmax(gain, idx);
+    if (idx == INT_MAX) return false;
+    const int start = idx;
+    int* mv_v = s.i32;
+    int* mv_src = s.i32 + k;
+    int* mv_dst = s.i32 + 2 * k;
+    int* ctl = s.i32 + 3 * k;  // [0]=nm [1]=natural [2]=cur [3]=done
+    double* steps = s.f64;
+    double* closers = s.f64 + k + 1;
+    if (lane == 0) {
+        ctl[0] = 0;
+        ctl[1] = 0;
+        ctl[2] = start;
+        ctl[3] = 0;
+    }
+    __syncwarp();
+    for (int it = 0; it < k; it++) {
+        if (lane == 0) {
+            int cur = ctl[2];
+            double home;
+            int v = fastest_free(s, cur, home);
+            if (v < 0) {
+                ctl[3] = 1;
+            } else {
+                int dst = -1;
+                double sc = -kInf;
+                for (int j = 0; j < k; j++) {
+                    if (j == cur) continue;
+                    double x = s.mean[v * k + j];
+                    if (dst < 0 || x > sc) {
+                        sc = x;
+                        dst = j;
+                    }
+                }
+                int nm = ctl[0];
+                closers[nm] = cur != start ? s.mean[v * k + start] - home : -kInf;
+                steps[nm] = sc - home;
+                g_remove(s, cur, v);  // _move (:294-296)
+                g_insort(s, dst, v);
+                s.locked[v >> 5] |= 1u << (v & 31);
+                s.nlocked[0]++;
+                mv_v[nm] = v;
+                mv_src[nm] = cur;
+                mv_dst[nm] = dst;
+                ctl[0] = nm + 1;
+                ctl[2] = dst;
+                s.valid[0] &= ~((1 << cur) | (1 << dst));
+                s.valid[1] &= ~((1 << cur) | (1 << dst));
+                if (dst == start) {
+                    ctl[1] = 1;
+                    ctl[3] = 1;
+                }
+            }
+        }
+        __syncwarp();
+        // refresh the touched mean columns and home costs (scheduler.py:362-363)
+        ensure_caches(s, lane);
+        if (ctl[3]) break;
+    }
+    const int nm = ctl[0];
+    if (nm == 0) return false;
+    bool applied = false;
+    if (lane == 0) {
+        double prefix = 0.0, best_v = -kInf;
+        int best_l = -1;
+        // prefix[l] = cumsum of steps[0..l-1] (np.cumsum, sequential)
+        for (int l = 0; l < nm; l++) {
+            double value = prefix + closers[l];
+            if (value > best_v) {
+                best_v = value;
+                best_l = l;
+            }
+            prefix = prefix + steps[l];
+        }
+        if (ctl[1] && prefix > best_v) {
+            best_v = prefix;
+            best_l = nm;
+        }
+        if (best_v <= 0.0) {
+            for (int t = nm - 1; t >= 0; t--) {
+                g_remove(s, mv_dst[t], mv_v[t]);
+                g_insort(s, mv_src[t], mv_v[t]);
+            }
+        } else {
+            for (int t = nm - 1; t >= best_l; t--) {
+                g_remove(s, mv_dst[t], mv_v[t]);
+                g_insort(s, mv_src[t], mv_v[t]);
+            }
+            if (best_l < nm) {
+                g_remove(s, mv_src[best_l], mv_v[best_l]);
+                g_insort(s, start, mv_v[best_l]);
+            }
+            applied = true;
+        }
+        for (int t = 0; t < nm; t++) {
+            invalidate(s, mv_src[t]);
+            invalidate(s, mv_dst[t]);
+        }
+        invalidate(s, start);
+        ctl[4] = applied;
+    }
+    __syncwarp();
+    return ctl[4] != 0;
+}
+
+// odd phase of _pass_ours: chains until every device is locked
+__device__ __noinline__ bool pass_chains(LS& s, int lane) {
+    const int n = s.n;
+    for (int i = lane; i < ((n + 31) >> 5); i += kWarp) s.locked[i] = 0;
+    if (lane == 0) s.nlocked[0] = 0;
+    __syncwarp();
+    bool changed = false;
+    while (s.nlocked[0] < n) {
+        int before = s.nlocked[0];
+        if (chain_round(s, lane)) changed = true;
+        __syncwarp();
+        if (s.nlocked[0] == before) break;
+    }
+    return changed;
+}
+
+// _pass_kl (:431-449)
+__device__ __noinline__ bool pass_kl(LS& s, int lane) {
+    const int k = s.k, n = s.n;
+    bool changed = false;
+    double* s11 = s.f64;
+    double* s12 = s11 + s.cap;
+    double* s22 = s12 + s.cap;
+    double* s21 = s22 + s.cap;
+    for (int j = 0; j < k; j++) {
+        for (int j2 = j + 1; j2 < k; j2++) {
+            const int16_t* a1 = s.G + j * s.cap;
+            const int16_t* a2 = s.G + j2 * s.cap;
+            const int c1 = s.sz[j], c2 = s.sz[j2];
+            for (int t = lane; t < 2 * (c1 + c2); t += kWarp) {
+                if (t < c1)
+                    s11[t] = row_pw(s, a1[t], a1, c1);
+                else if (t < 2 * c1)
+                    s12[t - c1] = row_pw(s, a1[t - c1], a2, c2);
+                else if (t < 2 * c1 + c2)
+                    s22[t - 2 * c1] = row_pw(s, a2[t - 2 * c1], a2, c2);
+                else
+                    s21[t - 2 * c1 - c2] = row_pw(s, a2[t - 2 * c1 - c2], a1, c1);
+            }
+            __syncwarp();
+            double bg = -kInf;
+            int bt = INT_MAX;
+            for (int t = lane; t < c1 * c2; t += kWarp) {
+                int i = t / c2, l = t - (t / c2) * c2;
+                double gn = ((s12[i] - s11[i]) + (s21[l] - s22[l])) - 2.0 * s.W[(size_t)a1[i] * n + a2[l]];
+                if (bt == INT_MAX || gn > bg) {
+                    bg = gn;
+                    bt = t;
+                }
+            }
+            warp_argmax(bg, bt);
+            if (bg > 0.0) {
+                if (lane == 0) {
+                    int a = a1[bt / c2], b = a2[bt % c2];
+                    g_remove(s, j, a);
+                    g_remove(s, j2, b);
+                    g_insort(s, j2, a);
+                    g_insort(s, j, b);
+                    invalidate(s, j);
+                    invalidate(s, j2);
+                }
+                changed = true;
+            }
+            __syncwarp();
+        }
+    }
+    return changed;
+}
+
+__device__ __forceinline__ void load_groups(LS& s, const int16_t* p, int lane) {
+    for (int t = lane; t < s.k * s.m; t += kWarp) s.G[(t / s.m) * s.cap + t % s.m] = p[t];
+    if (lane < s.k) s.sz[lane] = s.m;
+    if (lane == 0) {
+        s.valid[0] = 0;
+        s.valid[1] = 0;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void store_groups(const LS& s, int16_t* p, int lane) {
+    for (int t = lane; t < s.k * s.m; t += kWarp) p[t] = s.G[(t / s.m) * s.cap + t % s.m];
+    __syncwarp();
+}
+
+// crossover (:139-174), lane 0 after a lane-parallel group-of map
+__device__ __noinline__ void crossover(LS& s, const int16_t* p1, const int16_t* p2, Pcg64& rng, int16_t* out, int lane) {
+    const int k = s.k, m = s.m;
+    for (int t = lane; t < k * m; t += kWarp) s.grp_of[p1[t]] = (int8_t)(t / m);
+    __syncwarp();
+    if (lane == 0) {
+        int* slots = s.i32;       // k
+        int* cnt = s.i32 + k;     // k
+        int16_t* diff = s.perm;   // m (reused)
+        int ns = 0;
+        for (int j = 0; j < k; j++) {
+            int c = 0;
+            for (int i = 0; i < m; i++)
+                if (s.grp_of[p2[j * m + i]] != j) c++;
+            cnt[j] = c;
+            if (c) slots[ns++] = j;
+        }
+        if (ns == 0) {
+            for (int t = 0; t < k * m; t++) out[t] = p1[t];
+        } else {
+            int j = slots[rng.integers(0, ns)];
+            int nd = 0;
+            for (int i = 0; i < m; i++) {
+                int d = p2[j * m + i];
+                if (s.grp_of[d] != j) diff[nd++] = (int16_t)d;
+            }
+            int mi = (int)rng.integers(1, nd + 1);
+            // choice(nd, mi, replace=False): Floyd, then the shuffle's draws
+            int picked[64];
+            int np = 0;
+            for (int jj = nd - mi; jj < nd; jj++) {
+                int v = (int)rng.bounded((uint64_t)jj);
+                bool dup = false;
+                for (int t = 0; t < np; t++) dup |= picked[t] == v;
+                picked[np++] = dup ? jj : v;
+            }
+            for (int i = mi - 1; i >= 1; i--) (void)rng.bounded((uint64_t)i);
+            for (int a = 1; a < np; a++) {  // sorted(picked)
+                int x = picked[a], b = a - 1;
+                while (b >= 0 && picked[b] > x) {
+                    picked[b + 1] = picked[b];
+                    b--;
+                }
+                picked[b + 1] = x;
+            }
+            for (int t = 0; t < k * m; t++) s.G[(t / m) * s.cap + t % m] = p1[t];
+            for (int t = 0; t < k; t++) s.sz[t] = m;
+            int16_t pool[64];
+            int npool = m;
+            for (int i = 0; i < m; i++) pool[i] = p1[j * m + i];
+            for (int t = 0; t < mi; t++) {
+                int d = diff[picked[t]];
+                int src = s.grp_of[d];
+                g_remove(s, src, d);
+                g_insort(s, j, d);
+                s.grp_of[d] = (int8_t)j;
+                int vi = (int)rng.integers(0, npool);
+                int victim = pool[vi];
+                for (int q = vi; q + 1 < npool; q++) pool[q] = pool[q + 1];
+                npool--;
+                g_remove(s, j, victim);
+                g_insort(s, src, victim);
+                s.grp_of[victim] = (int8_t)src;
+            }
+            for (int t = 0; t < k * m; t++) out[t] = s.G[(t / m) * s.cap + t % m];
+        }
+    }
+    __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// the GA kernel
+
+struct GASmem {
+    LS ls;
+    int16_t* snaps;     // max_snaps x km
+    double* snapcost;   // max_snaps
+    double* popcost;    // P
+    int16_t* best;      // km
+    int16_t* par;       // 2 x km (parents)
+    int* ctl;           // [0] nsnap [1] stop [2] gen
+};
+
+__device__ __forceinline__ void copy16(int16_t* d, const int16_t* s, int n, int lane) {
+    for (int t = lane; t < n; t += kWarp) d[t] = s[t];
+}
+
+// Prices candidates cand[0..cnt) (smem, km each) round-robin over the CTA's
+// warps; cost[i] = datap + pipelinep.
+template <typename KeyT, bool kM8>
+__device__ __noinline__ void price_all(const EvalView<KeyT>& v, const WarpScratch& ws, const int16_t* cand,
+                                          int cnt, int km, double* cost, int wid, int W, int lane) {
+    for (int i = wid; i < cnt; i += W) {
+        double dp, pp;
+        warp_price<KeyT, kM8>(v, ws, cand + (size_t)i * km, lane, dp, pp);
+        if (lane == 0) cost[i] = dp + pp;
+        __syncwarp();
+    }
+}
+
+template <bool kSmemTables, typename KeyT, bool kM8>
+__global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int isl = blockIdx.x;
+    const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m, P = a.pop, cap = m + 1;
+    const int max_snaps = 1 + a.max_passes;
+    HKSmem hk = hk_stage(a.hk, smem);
+    size_t off = hk_smem_bytes(a.hk);
+    EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
+    const double* SW;
+    if (kSmemTables) {
+        double* ssw = reinterpret_cast<double*>(smem + off);
+        off += (size_t)n * n * 8;
+        for (int i = threadIdx.x; i < n * n; i += blockDim.x) ssw[i] = a.sw[i];
+        SW = ssw;
+    } else {
+        SW = a.sw;
+    }
+    WarpScratch ws = scratch_at(smem + off + (size_t)wid * wl.bytes, wl);
+    off += (size_t)W * wl.bytes;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = smem + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    GASmem g;
+    g.snaps = reinterpret_cast<int16_t*>(take((size_t)max_snaps * km * 2));
+    g.snapcost = reinterpret_cast<double*>(take((size_t)max_snaps * 8));
+    g.popcost = reinterpret_cast<double*>(take((size_t)P * 8));
+    g.best = reinterpret_cast<int16_t*>(take((size_t)km * 2));
+    g.par = reinterpret_cast<int16_t*>(take((size_t)2 * km * 2));
+    g.ctl = reinterpret_cast<int*>(take(16 * 4));
+    LS& s = g.ls;
+    s.n = n;
+    s.k = k;
+    s.m = m;
+    s.cap = cap;
+    s.W = SW;
+    s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
+    s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
+    s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
+    s.home = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.valid = reinterpret_cast<int*>(take(8));
+    s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
+    s.nlocked = reinterpret_cast<int*>(take(4));
+    s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
+    s.f64 = reinterpret_cast<double*>(take((size_t)(4 * cap + 2 * k + 2) * 8));
+    s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
+    s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+    __syncthreads();
+
+    __shared__ GAState st;
+    if (threadIdx.x == 0) st = a.state[isl];
+    __syncthreads();
+    int16_t* pop = a.pop_buf + (size_t)isl * P * km;
+    double* gcost = a.cost_buf + (size_t)isl * P;
+    int16_t* gbest = a.best_buf + (size_t)isl * km;
+    Pcg64 rng;
+    if (wid == 0) rng.load(st.rng);
+    const bool driver = wid == 0;
+
+    if (!st.initialized) {
+        // init_population (scheduler.py:124-136): sequential random_partition
+        // draws, then price every member (:537-542)
+        if (driver) {
+            for (int i = 0; i < P; i++) {
+                int16_t* dst = g.snaps;  // scratch
+                if (lane == 0) {
+                    for (int t = 0; t < n; t++) dst[t] = (int16_t)t;
+                    for (int t = n - 1; t >= 1; t--) {
+                        int jx = (int)rng.interval((uint64_t)t);
+                        int16_t x = dst[t];
+                        dst[t] = dst[jx];
+                        dst[jx] = x;
+                    }
+                }
+                __syncwarp();
+                if (lane < k) {  // Partition sorts members
+                    int16_t* gp = dst + lane * m;
+                    for (int aa = 1; aa < m; aa++) {
+                        int16_t x = gp[aa];
+                        int b = aa - 1;
+                        while (b >= 0 && gp[b] > x) {
+                            gp[b + 1] = gp[b];
+                            b--;
+                        }
+                        gp[b + 1] = x;
+                    }
+                }
+                __syncwarp();
+                copy16(pop + (size_t)i * km, dst, km, lane);
+                __syncwarp();
+            }
+        }
+        __threadfence_block();
+        __syncthreads();
+        // price the population in chunks of max_snaps through smem
+        for (int c0 = 0; c0 < P; c0 += max_snaps) {
+            int cnt = min(max_snaps, P - c0);
+            for (int t = threadIdx.x; t < cnt * km; t += blockDim.x) g.snaps[t] = pop[(size_t)c0 * km + t];
+            __syncthreads();
+            price_all<KeyT, kM8>(v, ws, g.snaps, cnt, km, g.popcost + c0, wid, W, lane);
+            __syncthreads();
+        }
+        if (driver) {
+            if (lane == 0) {
+                int bi = 0;
+                for (int i = 1; i < P; i++)
+                    if (g.popcost[i] < g.popcost[bi]) bi = i;  // min by (total, index)
+                st.best_total = g.popcost[bi];
+                st.best_idx = bi;
+                st.since = 0;
+                st.evaluations = P;
+                st.gen = 0;
+                st.stopped = 0;
+                st.initialized = 1;
+            }
+            __syncwarp();
+            copy16(gbest, pop + (size_t)st.best_idx * km, km, lane);
+        }
+    } else {
+        for (int t = threadIdx.x; t < P; t += blockDim.x) g.popcost[t] = gcost[t];
+    }
+    if (driver && lane == 0) {
+        g.ctl[1] = st.stopped;
+        g.ctl[2] = st.gen;
+    }
+    __threadfence_block();
+    __syncthreads();
+
+    const int gen_end = min(a.gen_end, a.generations);
+    const int stop_after = a.kind == 0 ? 2 : 1;
+    while (!g.ctl[1] && g.ctl[2] < gen_end) {
+        const int gen = g.ctl[2];
+        if (driver) {
+            int i = 0, i2 = 0;
+            if (lane == 0) {
+                i = (int)rng.integers(0, P);
+                i2 = (int)rng.integers(0, P - 1);
+                if (i2 >= i) i2++;
+            }
+            i = __shfl_sync(kFull, i, 0);
+            i2 = __shfl_sync(kFull, i2, 0);
+            copy16(g.par, pop + (size_t)i * km, km, lane);
+            copy16(g.par + km, pop + (size_t)i2 * km, km, lane);
+            __syncwarp();
+            crossover(s, g.par, g.par + km, rng, g.snaps, lane);
+            int nsnap = 1;
+            if (a.kind != 2) {  // _refine (:455-487)
+                load_groups(s, g.snaps, lane);
+                int stale = 0;
+                for (int t = 0; t < a.max_passes; t++) {
+                    bool changed;
+                    if (a.kind == 0)
+                        changed = (s.sz[0] < 2) ? false : (t % 2 == 0 ? pass_sweep(s, rng, lane) : pass_chains(s, lane));
+                    else
+                        changed = pass_kl(s, lane);
+                    if (!changed) {
+                        stale++;
+                        if (stale >= stop_after) break;
+                        continue;
+                    }
+                    stale = 0;
+                    store_groups(s, g.snaps + (size_t)nsnap * km, lane);
+                    nsnap++;
+                }
+            }
+            if (lane == 0) g.ctl[0] = nsnap;
+        }
+        __syncthreads();
+        const int nsnap = g.ctl[0];
+        price_all<KeyT, kM8>(v, ws, g.snaps, nsnap, km, g.snapcost, wid, W, lane);
+        __syncthreads();
+        if (driver) {
+            int bsi = 0, worst = 0, replace = 0, improve = 0;
+            double cb = 0.0;
+            if (lane == 0) {
+                for (int q = 1; q < nsnap; q++)
+                    if (g.snapcost[q] < g.snapcost[bsi]) bsi = q;  // first strict minimum
+                cb = g.snapcost[bsi];
+                st.evaluations += nsnap;
+                for (int t = 1; t < P; t++)
+                    if (g.popcost[t] > g.popcost[worst]) worst = t;  // first maximum
+                replace = cb < g.popcost[worst];
+                improve = cb < st.best_total;
+                if (replace) g.popcost[worst] = cb;
+                if (improve) {
+                    st.best_total = cb;
+                    st.since = 0;
+                } else {
+                    st.since++;
+                }
+            }
+            bsi = __shfl_sync(kFull, bsi, 0);
+            worst = __shfl_sync(kFull, worst, 0);
+            replace = __shfl_sync(kFull, replace, 0);
+            improve = __shfl_sync(kFull, improve, 0);
+            const int16_t* refined = g.snaps + (size_t)bsi * km;
+            if (replace) copy16(pop + (size_t)worst * km, refined, km, lane);
+            if (improve) copy16(gbest, refined, km, lane);
+            __syncwarp();
+            if (lane == 0) {
+                if (a.trace_best) a.trace_best[(size_t)isl * a.generations + gen] = st.best_total;
+                if (a.trace_mean) a.trace_mean[(size_t)isl * a.generations + gen] = pw_array(g.popcost, P) / (double)P;
+                st.gen = gen + 1;
+                g.ctl[2] = gen + 1;
+                if (a.patience > 0 && st.since >= a.patience) {
+                    st.stopped = 1;
+                    g.ctl[1] = 1;
+                }
+            }
+        }
+        __threadfence_block();
+        __syncthreads();
+    }
+
+    // persist population costs; finalize when the run is over
+    for (int t = threadIdx.x; t < P; t += blockDim.x) gcost[t] = g.popcost[t];
+    bool finished = g.ctl[1] || g.ctl[2] >= a.generations;
+    if (finished && a.finalize && !st.finalized) {
+        // canonical() (costmodel.py:86-88) then a last priced evaluation (:572-574)
+        if (driver) {
+            if (lane == 0) {
+                int ord[16];
+                for (int j = 0; j < k; j++) ord[j] = j;
+                for (int x = 1; x < k; x++) {
+                    int y = ord[x], b = x - 1;
+                    while (b >= 0 && gbest[ord[b] * m] > gbest[y * m]) {
+                        ord[b + 1] = ord[b];
+                        b--;
+                    }
+                    ord[b + 1] = y;
+                }
+                for (int j = 0; j < k; j++)
+                    for (int i = 0; i < m; i++) g.snaps[j * m + i] = gbest[ord[j] * m + i];
+            }
+            __syncwarp();
+            double dp, pp;
+            warp_price<KeyT, kM8>(v, ws, g.snaps, lane, dp, pp);
+            if (lane == 0) {
+                st.evaluations += 1;
+                a.out3[isl * 3 + 0] = dp + pp;
+                a.out3[isl * 3 + 1] = dp;
+                a.out3[isl * 3 + 2] = pp;
+                if (a.out_order) held_karp_order(k, ws.E, ws.h, hk.hoff, pp, a.out_order + (size_t)isl * k);
+            }
+            if (lane < k && a.out_pg) a.out_pg[(size_t)isl * k + lane] = ws.pg[lane];
+            copy16(a.out_groups + (size_t)isl * km, g.snaps, km, lane);
+            if (lane == 0) st.finalized = 1;
+        }
+    }
+    __syncthreads();
+    if (driver && lane == 0) {
+        rng.store(st.rng);
+        a.state[isl] = st;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// local_search (scheduler.py:490-512): _refine on a batch of partitions, one
+// CTA each with its own PCG64 stream; returns the best truly-priced layout.
+
+template <bool kSmemTables, typename KeyT, bool kM8>
+__global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout wl) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int b = blockIdx.x;
+    const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m, cap = m + 1;
+    const int max_snaps = 1 + a.max_passes;
+    HKSmem hk = hk_stage(a.hk, smem);
+    size_t off = hk_smem_bytes(a.hk);
+    EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
+    const double* SW;
+    if (kSmemTables) {
+        double* ssw = reinterpret_cast<double*>(smem + off);
+        off += (size_t)n * n * 8;
+        for (int i = threadIdx.x; i < n * n; i += blockDim.x) ssw[i] = a.sw[i];
+        SW = ssw;
+    } else {
+        SW = a.sw;
+    }
+    WarpScratch ws = scratch_at(smem + off + (size_t)wid * wl.bytes, wl);
+    off += (size_t)W * wl.bytes;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = smem + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    int16_t* snaps = reinterpret_cast<int16_t*>(take((size_t)max_snaps * km * 2));
+    double* snapcost = reinterpret_cast<double*>(take((size_t)max_snaps * 8));
+    int* ctl = reinterpret_cast<int*>(take(16 * 4));
+    LS s;
+    s.n = n;
+    s.k = k;
+    s.m = m;
+    s.cap = cap;
+    s.W = SW;
+    s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
+    s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
+    s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
+    s.home = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.valid = reinterpret_cast<int*>(take(8));
+    s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
+    s.nlocked = reinterpret_cast<int*>(take(4));
+    s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
+    s.f64 = reinterpret_cast<double*>(take((size_t)(4 * cap + 2 * k + 2) * 8));
+    s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
+    s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+    for (int t = threadIdx.x; t < km; t += blockDim.x) snaps[t] = a.groups[(size_t)b * km + t];
+    __syncthreads();
+    Pcg64 rng;
+    if (wid == 0) {
+        rng.load(a.rng[b]);
+        int nsnap = 1;
+        if (a.single_pass) {
+            load_groups(s, snaps, lane);
+            bool ch = a.kind == 0 ? ((s.sz[0] < 2) ? false : (a.phase % 2 == 0 ? pass_sweep(s, rng, lane) : pass_chains(s, lane)))
+                                  : pass_kl(s, lane);
+            store_groups(s, a.out_groups + (size_t)b * km, lane);
+            if (lane == 0) a.changed[b] = ch;
+        } else {
+            load_groups(s, snaps, lane);
+            int stale = 0, stop_after = a.kind == 0 ? 2 : 1;
+            for (int t = 0; t < a.max_passes; t++) {
+                bool changed = a.kind == 0 ? ((s.sz[0] < 2) ? false : (t % 2 == 0 ? pass_sweep(s, rng, lane) : pass_chains(s, lane)))
+                                           : pass_kl(s, lane);
+                if (!changed) {
+                    stale++;
+                    if (stale >= stop_after) break;
+                    continue;
+                }
+                stale = 0;
+                store_groups(s, snaps + (size_t)nsnap * km, lane);
+                nsnap++;
+            }
+        }
+        if (lane == 0) {
+            ctl[0] = nsnap;
+            rng.store(a.rng[b]);
+        }
+    }
+    __syncthreads();
+    if (a.single_pass) return;
+    const int nsnap = ctl[0];
+    price_all<KeyT, kM8>(v, ws, snaps, nsnap, km, snapcost, wid, W, lane);
+    __syncthreads();
+    if (wid == 0) {
+        int bsi = 0;
+        if (lane == 0)
+            for (int q = 1; q < nsnap; q++)
+                if (snapcost[q] < snapcost[bsi]) bsi = q;
+        bsi = __shfl_sync(kFull, bsi, 0);
+        copy16(a.out_groups + (size_t)b * km, snaps + (size_t)bsi * km, km, lane);
+        if (lane == 0) {
+            a.out_cost[b] = snapcost[bsi];
+            a.evaluations[b] = nsnap;
+        }
+    }
+}
+
+// crossover(p1, p2, rng) on a batch (one warp each)
+__global__ void crossover_kernel(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs,
+                                 int16_t* out, int B) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x;
+    if (b >= B) return;
+    const int km = k * m, cap = m + 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = smem + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    LS s;
+    s.n = n;
+    s.k = k;
+    s.m = m;
+    s.cap = cap;
+    s.W = nullptr;
+    s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
+    s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
+    s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
+    s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
+    s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+    int16_t* a1 = reinterpret_cast<int16_t*>(take((size_t)km * 2));
+    int16_t* a2 = reinterpret_cast<int16_t*>(take((size_t)km * 2));
+    int16_t* o = reinterpret_cast<int16_t*>(take((size_t)km * 2));
+    copy16(a1, p1 + (size_t)b * km, km, lane);
+    copy16(a2, p2 + (size_t)b * km, km, lane);
+    __syncwarp();
+    Pcg64 rng;
+    rng.load(rngs[b]);
+    crossover(s, a1, a2, rng, o, lane);
+    copy16(out + (size_t)b * km, o, km, lane);
+    if (lane == 0) rng.store(rngs[b]);
+}
+
+// gain_ours / gain_kl (scheduler.py:181-230) for a batch of queries, one
+// thread each; q = (j, j2, d1, d2, d1p, d2p) or (d, d2, jd, jd2).
+__global__ void gains_kernel(int n, int k, int m, const double* __restrict__ sw, const int16_t* __restrict__ groups,
+                             const int32_t* __restrict__ q, int kind, int B, double* __restrict__ out) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const int16_t* G = groups + (size_t)b * k * m;
+    const int32_t* Q = q + (size_t)b * 6;
+    auto psum = [&](int u, const int16_t* grp, int cnt, int skip) {
+        // numpy pairwise sum of w[u, grp] (optionally without member `skip`)
+        double buf[64];
+        int c = 0;
+        for (int i = 0; i < cnt; i++)
+            if (grp[i] != skip) buf[c++] = sw[(size_t)u * n + grp[i]];
+        return pairwise_sum(c, [&](int i) { return buf[i]; });
+    };
+    if (kind == 0) {
+        int j = Q[0], j2 = Q[1], d1 = Q[2], d2 = Q[3], d1p = Q[4], d2p = Q[5];
+        const int16_t* gj = G + j * m;
+        const int16_t* gj2 = G + j2 * m;
+        double t1 = psum(d1, gj2, m, -1) / (double)m - sw[(size_t)d1 * n + d2];
+        double t2 = psum(d1p, gj, m, -1) / (double)m - sw[(size_t)d1p * n + d2p];
+        out[b] = t1 + t2;
+    } else {
+        int d = Q[0], d2 = Q[1], jd = Q[2], jd2 = Q[3];
+        const int16_t* gj = G + jd * m;
+        const int16_t* gj2 = G + jd2 * m;
+        double t1 = psum(d, gj2, m, -1);
+        double t2 = psum(d, gj, m, d);
+        double t3 = psum(d2, gj, m, -1);
+        double t4 = psum(d2, gj2, m, d2);
+        out[b] = t1 - t2 + t3 - t4 - 2.0 * sw[(size_t)d * n + d2];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+static size_t ls_bytes(int n, int k, int m) {
+    int cap = m + 1;
+    auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)n * k * 8) + al((size_t)n * 8) + al(8) +
+           al((size_t)((n + 31) >> 5) * 4) + al(4) + al((size_t)(k * k + cap) * 2) +
+           al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
+}
+
+static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P) {
+    auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    ScratchLayout wl = scratch_layout(sh.k, sh.m);
+    int km = sh.k * sh.m, ms = 1 + sh.max_passes;
+    size_t b = hk_smem_bytes(sh.hk) + (size_t)W * wl.bytes;
+    if (smem_tables)
+        b += (size_t)sh.n * sh.n * 8 + al((size_t)sh.n * sh.n * (sh.key16 ? 2 : 4)) + (size_t)sh.n * sh.n * 8;
+    b += al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) + al((size_t)2 * km * 2) +
+         al(64);
+    b += ls_bytes(sh.n, sh.k, sh.m);
+    return b;
+}
+
+int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan) {
+    for (int W : {8, 6, 4, 2, 1}) {
+        for (int st = 1; st >= 0; st--) {
+            size_t b = ga_bytes(sh, W, st, P);
+            if (b <= smem_optin) {
+                plan->warps = W;
+                plan->smem_tables = st;
+                plan->smem = b;
+                plan->m8 = sh.key16 && sh.m == 8 && sh.nvals <= 0x8000;
+                return 0;
+            }
+        }
+    }
+    return -2;
+}
+
+template <bool S, typename KT, bool M8>
+static int launch_ga_t(const GAArgs& a, const SearchPlan& plan, int islands, cudaStream_t st) {
+    ScratchLayout wl = scratch_layout(a.k, a.m);
+    cudaFuncSetAttribute(ga_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    ga_kernel<S, KT, M8><<<islands, plan.warps * 32, plan.smem, st>>>(a, wl);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_ga(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st) {
+    if (plan.m8) return plan.smem_tables ? launch_ga_t<true, uint16_t, true>(a, plan, islands, st)
+                                         : launch_ga_t<false, uint16_t, true>(a, plan, islands, st);
+    if (key16) return plan.smem_tables ? launch_ga_t<true, uint16_t, false>(a, plan, islands, st)
+                                       : launch_ga_t<false, uint16_t, false>(a, plan, islands, st);
+    return plan.smem_tables ? launch_ga_t<true, uint32_t, false>(a, plan, islands, st)
+                            : launch_ga_t<false, uint32_t, false>(a, plan, islands, st);
+}
+
+template <bool S, typename KT, bool M8>
+static int launch_refine_t(const RefineArgs& a, const SearchPlan& plan, int B, cudaStream_t st) {
+    ScratchLayout wl = scratch_layout(a.k, a.m);
+    cudaFuncSetAttribute(refine_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    refine_kernel<S, KT, M8><<<B, plan.warps * 32, plan.smem, st>>>(a, wl);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_refine(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st) {
+    if (B == 0) return 0;
+    if (plan.m8) return plan.smem_tables ? launch_refine_t<true, uint16_t, true>(a, plan, B, st)
+                                         : launch_refine_t<false, uint16_t, true>(a, plan, B, st);
+    if (key16) return plan.smem_tables ? launch_refine_t<true, uint16_t, false>(a, plan, B, st)
+                                       : launch_refine_t<false, uint16_t, false>(a, plan, B, st);
+    return plan.smem_tables ? launch_refine_t<true, uint32_t, false>(a, plan, B, st)
+                            : launch_refine_t<false, uint32_t, false>(a, plan, B, st);
+}
+
+int launch_crossover(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs, int16_t* out, int B,
+                     cudaStream_t st) {
+    if (B == 0) return 0;
+    size_t smem = ls_bytes(n, k, m) + 3 * (((size_t)k * m * 2 + 15) & ~(size_t)15) + 256;
+    cudaFuncSetAttribute(crossover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    crossover_kernel<<<B, 32, smem, st>>>(n, k, m, p1, p2, rngs, out, B);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_gains(int n, int k, int m, const double* sw, const int16_t* groups, const int32_t* q, int kind, int B,
+                 double* out, cudaStream_t st) {
+    if (B == 0) return 0;
+    gains_kernel<<<(B + 127) / 128, 128, 0, st>>>(n, k, m, sw, groups, q, kind, B, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// ---------------------------------------------------------------------------
+// island migration (new capability)
+
+// export: each island's E best members by (cost, index), one warp per island
+__global__ void export_kernel(int P, int km, int E, const int16_t* __restrict__ pop, const double* __restrict__ cost,
+                              int16_t* __restrict__ out, double* __restrict__ out_cost) {
+    const int isl = blockIdx.x, lane = threadIdx.x;
+    const int16_t* ip = pop + (size_t)isl * P * km;
+    const double* ic = cost + (size_t)isl * P;
+    uint64_t taken[4] = {0, 0, 0, 0};  // P <= 256
+    for (int e = 0; e < E; e++) {
+        double bv = kInf;
+        int bi = INT_MAX;
+        for (int i = lane; i < P; i += kWarp)
+            if (!(taken[i >> 6] >> (i & 63) & 1) && (ic[i] < bv || (ic[i] == bv && i < bi))) {
+                bv = ic[i];
+                bi = i;
+            }
+        warp_argmin(bv, bi);
+        taken[bi >> 6] |= 1ull << (bi & 63);
+        copy16(out + ((size_t)isl * E + e) * km, ip + (size_t)bi * km, km, lane);
+        if (lane == 0) out_cost[(size_t)isl * E + e] = bv;
+    }
+}
+
+// import: island i receives migrants[src[i]]; each replaces the current
+// worst member (first maximum) when strictly cheaper, and may become best.
+__global__ void import_kernel(int P, int km, int E, int16_t* __restrict__ pop, double* __restrict__ cost,
+                              int16_t* __restrict__ best, GAState* __restrict__ state, const int16_t* __restrict__ mig,
+                              const double* __restrict__ mig_cost, const int32_t* __restrict__ src) {
+    const int isl = blockIdx.x, lane = threadIdx.x;
+    int16_t* ip = pop + (size_t)isl * P * km;
+    double* ic = cost + (size_t)isl * P;
+    const int s = src[isl];
+    for (int e = 0; e < E; e++) {
+        const int16_t* g = mig + ((size_t)s * E + e) * km;
+        double c = mig_cost[(size_t)s * E + e];
+        double wv = -kInf;
+        int wi = INT_MAX;
+        for (int i = lane; i < P; i += kWarp)
+            if (ic[i] > wv || (ic[i] == wv && i < wi)) {
+                wv = ic[i];
+                wi = i;
+            }
+        warp_argmax(wv, wi);
+        if (c < wv) {
+            copy16(ip + (size_t)wi * km, g, km, lane);
+            __syncwarp();
+            if (lane == 0) ic[wi] = c;
+        }
+        if (c < state[isl].best_total) {
+            copy16(best + (size_t)isl * km, g, km, lane);
+            __syncwarp();
+            if (lane == 0) {
+                state[isl].best_total = c;
+                state[isl].since = 0;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// init_population draws from one stream (lane 0), then lanes sort groups
+__global__ void random_partitions_kernel(int n, int k, int m, int B, hs_pcg64* rng_io, int16_t* out) {
+    const int lane = threadIdx.x;
+    Pcg64 rng;
+    if (lane == 0) rng.load(*rng_io);
+    for (int b = 0; b < B; b++) {
+        int16_t* d = out + (size_t)b * n;
+        if (lane == 0) {
+            for (int t = 0; t < n; t++) d[t] = (int16_t)t;
+            for (int t = n - 1; t >= 1; t--) {
+                int jx = (int)rng.interval((uint64_t)t);
+                int16_t x = d[t];
+                d[t] = d[jx];
+                d[jx] = x;
+            }
+        }
+        __syncwarp();
+        for (int j = lane; j < k; j += kWarp) {
+            int16_t* gp = d + j * m;
+            for (int a = 1; a < m; a++) {
+                int16_t x = gp[a];
+                int q = a - 1;
+                while (q >= 0 && gp[q] > x) {
+                    gp[q + 1] = gp[q];
+                    q--;
+                }
+                gp[q + 1] = x;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) rng.store(*rng_io);
+}
+
+int launch_export(int islands, int P, int km, int E, const int16_t* pop, const double* cost, int16_t* out,
+                  double* out_cost, cudaStream_t st) {
+    export_kernel<<<islands, 32, 0, st>>>(P, km, E, pop, cost, out, out_cost);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_import(int islands, int P, int km, int E, int16_t* pop, double* cost, int16_t* best, GAState* state,
+                  const int16_t* mig, const double* mig_cost, const int32_t* src, cudaStream_t st) {
+    import_kernel<<<islands, 32, 0, st>>>(P, km, E, pop, cost, best, state, mig, mig_cost, src);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_random_partitions(int n, int k, int m, int B, hs_pcg64* rng, int16_t* out, cudaStream_t st) {
+    random_partitions_kernel<<<1, 32, 0, st>>>(n, k, m, B, rng, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace hs

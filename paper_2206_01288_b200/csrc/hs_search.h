@@ -1,0 +1,83 @@
+// hs_search.h -- host/device interface of the search kernels (K2/K3).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/hetsched_b200.h"
+#include "hs_internal.h"
+
+namespace hs {
+
+// Per-island GA state kept in global memory between launches (epochs).
+struct GAState {
+    hs_pcg64 rng;
+    double best_total;
+    long long evaluations;
+    int best_idx, since, gen, stopped, initialized, finalized;
+};
+
+struct GAArgs {
+    int n, k, m;
+    const double* sw;
+    const double* dp;
+    const void* rank;
+    const double* vals;
+    HKTables hk;
+    int pop, generations, kind /*0 ours 1 kl 2 none*/, max_passes, patience /*<=0: none*/;
+    int gen_end;   // run generations [state.gen, gen_end)
+    int finalize;  // price the canonical best when the run is over
+    GAState* state;      // [islands]
+    int16_t* pop_buf;    // [islands][pop][k*m]
+    double* cost_buf;    // [islands][pop]
+    int16_t* best_buf;   // [islands][k*m]
+    double* trace_best;  // [islands][generations] (nullable)
+    double* trace_mean;
+    double* out3;        // [islands][3] total, datap, pipelinep
+    double* out_pg;      // [islands][k]
+    int8_t* out_order;   // [islands][k]
+    int16_t* out_groups; // [islands][k*m] canonical best
+};
+
+struct RefineArgs {
+    int n, k, m;
+    const double* sw;
+    const double* dp;
+    const void* rank;
+    const double* vals;
+    HKTables hk;
+    int kind, max_passes, single_pass, phase;
+    const int16_t* groups;  // [B][k*m]
+    hs_pcg64* rng;          // [B] in/out
+    int16_t* out_groups;    // [B][k*m]
+    double* out_cost;       // [B]
+    int* evaluations;       // [B]
+    int* changed;           // [B] (single_pass)
+};
+
+struct SearchShape {
+    int n, k, m, max_passes, nvals;
+    bool key16;
+    HKTables hk;
+};
+
+struct SearchPlan {
+    int warps;
+    bool smem_tables, m8;
+    size_t smem;
+};
+
+int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan);
+int launch_ga(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st);
+int launch_refine(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st);
+int launch_crossover(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs, int16_t* out, int B,
+                     cudaStream_t st);
+int launch_gains(int n, int k, int m, const double* sw, const int16_t* groups, const int32_t* q, int kind, int B,
+                 double* out, cudaStream_t st);
+
+int launch_export(int islands, int P, int km, int E, const int16_t* pop, const double* cost, int16_t* out,
+                  double* out_cost, cudaStream_t st);
+int launch_import(int islands, int P, int km, int E, int16_t* pop, double* cost, int16_t* best, GAState* state,
+                  const int16_t* mig, const double* mig_cost, const int32_t* src, cudaStream_t st);
+int launch_random_partitions(int n, int k, int m, int B, hs_pcg64* rng, int16_t* out, cudaStream_t st);
+
+}  // namespace hs

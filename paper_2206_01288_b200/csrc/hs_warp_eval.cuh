@@ -1,0 +1,203 @@
+// hs_warp_eval.cuh -- one warp prices one candidate layout (comm_cost,
+// costmodel.py:217-229).  Shared by the batch evaluator (K1) and the GA
+// kernel (K3), so both produce the same bits.
+#pragma once
+#include "hs_eval.cuh"
+#include "hs_internal.h"
+
+namespace hs {
+
+// Per-CTA copy of the Held-Karp state list and compact offsets.
+struct HKSmem {
+    const uint32_t* states;
+    const int* lay;
+    const uint16_t* hoff;
+};
+
+__host__ __device__ __forceinline__ size_t hk_smem_bytes(const HKTables& t) {
+    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
+}
+
+__device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* base) {
+    uint32_t* st = reinterpret_cast<uint32_t*>(base);
+    size_t off = ((size_t)t.nstates * 4 + 15) & ~(size_t)15;
+    int* lay = reinterpret_cast<int*>(base + off);
+    off += 80;
+    uint16_t* hoff = reinterpret_cast<uint16_t*>(base + off);
+    for (int i = threadIdx.x; i < t.nstates; i += blockDim.x) st[i] = t.states[i];
+    for (int i = threadIdx.x; i < t.nhoff; i += blockDim.x) hoff[i] = t.hoff[i];
+    if (threadIdx.x < 18) lay[threadIdx.x] = t.lay[threadIdx.x];
+    return HKSmem{st, lay, hoff};
+}
+
+// What a warp reads to price a candidate (tables in smem or global).
+template <typename KeyT>
+struct EvalView {
+    int n, k, m;
+    const double* DP;
+    const KeyT* RK;
+    const double* vals;
+    HKSmem hk;
+};
+
+// Per-warp scratch: h holds max(k*2^(k-1) - k, k*m) doubles (row sums,
+// then the Held-Karp table), E the padded k x k stage graph.
+struct WarpScratch {
+    double* h;
+    double* E;
+    double* pg;
+    uint32_t* seen;
+};
+
+struct ScratchLayout {
+    int h_off, e_off, pg_off, mem_off, seen_off, bytes;
+};
+
+__host__ __device__ inline ScratchLayout scratch_layout(int k, int m) {
+    ScratchLayout wl;
+    int km = k * m;
+    int hk = (k << (k - 1)) - k;
+    int hsz = hk > km ? hk : km;
+    int o = 0;
+    wl.h_off = o;
+    o += hsz * 8;
+    wl.e_off = o;
+    o += 8 * kES * 8;
+    wl.pg_off = o;
+    o += 8 * 8;
+    wl.mem_off = o;
+    o += (km * 2 + 15) & ~15;
+    wl.seen_off = o;
+    o += 32 * 4;
+    wl.bytes = (o + 15) & ~15;
+    return wl;
+}
+
+__device__ __forceinline__ WarpScratch scratch_at(unsigned char* wbase, const ScratchLayout& wl) {
+    return WarpScratch{reinterpret_cast<double*>(wbase + wl.h_off), reinterpret_cast<double*>(wbase + wl.e_off),
+                       reinterpret_cast<double*>(wbase + wl.pg_off), reinterpret_cast<uint32_t*>(wbase + wl.seen_off)};
+}
+
+__device__ __forceinline__ void decode_pair(int t, int k, int& j, int& j2) {
+    j = 0;
+    while (t >= k - 1 - j) {
+        t -= k - 1 - j;
+        j++;
+    }
+    j2 = j + 1 + t;
+}
+
+// Partition invariants (costmodel.py:58-72): in range, ascending within each
+// group, covering 0..n-1 (k*m == n, so covering implies disjoint).
+__device__ inline bool warp_valid(int n, int k, int m, const int16_t* mem, uint32_t* seen, int lane) {
+    const int km = k * m, nwords = (n + 31) >> 5;
+    for (int i = lane; i < nwords; i += kWarp) seen[i] = 0;
+    __syncwarp();
+    bool bad = false;
+    for (int i = lane; i < km; i += kWarp) {
+        int d = mem[i];
+        if (d < 0 || d >= n) {
+            bad = true;
+        } else {
+            if (i % m != 0 && mem[i - 1] >= d) bad = true;
+            atomicOr(&seen[d >> 5], 1u << (d & 31));
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < nwords; i += kWarp) {
+        int bits = min(32, n - i * 32);
+        uint32_t want = bits == 32 ? 0xffffffffu : ((1u << bits) - 1u);
+        if (seen[i] != want) bad = true;
+    }
+    return !__any_sync(0xffffffffu, bad);
+}
+
+// Prices the partition in mem[k*m] (smem, members ascending).  All lanes
+// return the same (datap, pipe); total = datap + pipe.  Afterwards s.pg holds
+// per_group_datap and s.h / s.E the Held-Karp table for order reconstruction.
+template <typename KeyT, bool kM8>
+__device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s, const int16_t* mem, int lane,
+                                  double& datap, double& pipe) {
+    const int n = v.n, k = v.k, m = kM8 ? 8 : v.m, km = k * m;
+    double* h = s.h;
+    double* E = s.E;
+    // data-parallel level (costmodel.py:154-175): numpy pairwise row sums over
+    // the sorted members (diagonal 0.0 in its slot), max per group
+    for (int r = lane; r < km; r += kWarp) {
+        int g = r / m;
+        const int16_t* gm = mem + g * m;
+        const double* row = v.DP + (size_t)gm[r - g * m] * n;
+        h[r] = pairwise_sum(m, [&](int c) { return row[gm[c]]; });
+    }
+    __syncwarp();
+    if (lane < k) {
+        double mx = h[lane * m];
+        for (int i = 1; i < m; i++) mx = dmax(mx, h[lane * m + i]);
+        s.pg[lane] = mx;
+    }
+    // pipeline edges (costmodel.py:200-208): bottleneck of each group pair
+    const int npairs = k * (k - 1) / 2;
+    for (int t = lane; t < npairs; t += kWarp) {
+        int j, j2;
+        decode_pair(t, k, j, j2);
+        const int16_t* A = mem + j * m;
+        const int16_t* B = mem + j2 * m;
+        uint32_t L;
+        if (kM8) {
+            int b[8];
+#pragma unroll
+            for (int c = 0; c < 8; c++) b[c] = B[c];
+            uint32_t K[8][4];
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                const KeyT* row = v.RK + (size_t)A[r] * n;
+#pragma unroll
+                for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
+            }
+            L = Match8::solve(K);
+        } else {
+            L = bottleneck_threshold<uint32_t>(
+                m, [&](int r, int c) { return (uint32_t)v.RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
+        }
+        double val = v.vals[L];
+        E[j * kES + j2] = val;
+        E[j2 * kES + j] = val;
+    }
+    if (lane < k) E[lane * kES + lane] = 0.0;
+    __syncwarp();
+    pipe = warp_held_karp(k, E, h, v.hk.states, v.hk.lay, lane);
+    double dp = s.pg[0];
+    for (int g = 1; g < k; g++) dp = dmax(dp, s.pg[g]);
+    datap = dp;
+}
+
+// Stage DP and the rank table into smem (or point at global copies).
+template <bool kSmemTables, typename KeyT>
+__device__ inline EvalView<KeyT> stage_tables(int n, int k, int m, const double* dp, const void* rank,
+                                              const double* vals, HKSmem hk, unsigned char* smem, size_t& off) {
+    EvalView<KeyT> v;
+    v.n = n;
+    v.k = k;
+    v.m = m;
+    v.vals = vals;
+    v.hk = hk;
+    const KeyT* grk = reinterpret_cast<const KeyT*>(rank);
+    if (kSmemTables) {
+        double* sdp = reinterpret_cast<double*>(smem + off);
+        off += (size_t)n * n * 8;
+        KeyT* srk = reinterpret_cast<KeyT*>(smem + off);
+        off += ((size_t)n * n * sizeof(KeyT) + 15) & ~(size_t)15;
+        for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+            sdp[i] = dp[i];
+            srk[i] = grk[i];
+        }
+        v.DP = sdp;
+        v.RK = srk;
+    } else {
+        v.DP = dp;
+        v.RK = grk;
+    }
+    return v;
+}
+
+}  // namespace hs

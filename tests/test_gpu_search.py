@@ -1,0 +1,214 @@
+"""GPU parity of the search path (K2 gains / local search, K3 GA) through the C-ABI.
+
+Bitwise against the golden vectors the reference produced and, at larger
+scale, against the oracle; RNG states must come back advanced exactly as
+numpy would advance them.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests import _instances as I
+from tests._instances import fx
+
+pytestmark = pytest.mark.gpu
+
+hs = pytest.importorskip("paper_2206_01288_b200")
+from paper_2206_01288_b200 import scheduler as S  # noqa: E402
+
+
+def _rng_tuple(rng):
+    st = rng.bit_generator.state
+    return [str(st["state"]["state"]), st["has_uint32"], st["uinteger"]]
+
+
+def _gpu_ok(name):
+    k, m = I.meta()[name]["recipe"]["w"][:2]
+    return k <= 8 and m <= 64
+
+
+def test_surrogate_weights_and_g4_gains():
+    g, w = I.instance("g4")
+    sw = S.SurrogateWeights.from_instance(g, w)
+    assert sw.w[0, 1] == pytest.approx(0.501, rel=1e-12) and sw.w[0, 2] == pytest.approx(5.05, rel=1e-12)
+    good, bad = hs.Partition(((0, 1), (2, 3))), hs.Partition(((0, 2), (1, 3)))
+    assert S.gain_ours(sw, bad, 0, 1, (0, 2, 1, 3)) == pytest.approx(-4.549, rel=1e-9)
+    assert S.gain_ours(sw, good, 0, 1, (0, 1, 2, 3)) == pytest.approx(9.098, rel=1e-9)
+    assert S.gain_kl(sw, good, 0, 2) == pytest.approx(9.098, rel=1e-9)
+    with pytest.raises(S.ScheduleError, match="both in group 0"):
+        S.gain_kl(sw, good, 0, 1)
+
+
+def test_gains_match_golden():
+    for c in I.fixture("search.json")["gains"]:
+        g, w = I.instance(c["inst"])
+        sw = S.SurrogateWeights.from_instance(g, w)
+        p = hs.Partition.from_groups(c["groups"])
+        if c["kind"] == "ours":
+            j, j2, *cand = c["args"]
+            v = S.gain_ours(sw, p, j, j2, tuple(cand))
+        else:
+            v = S.gain_kl(sw, p, *c["args"])
+        assert v == fx(c["value"]), c
+
+
+def test_gain_kl_equals_cut_difference_dyadic():
+    rng = np.random.default_rng(0)
+    for _ in range(50):
+        raw = rng.integers(0, 256, size=(12, 12)).astype(float)
+        wm = (raw + raw.T) / 16.0
+        np.fill_diagonal(wm, 0.0)
+        sw = S.SurrogateWeights(wm)
+        perm = rng.permutation(12)
+        p = hs.Partition.from_groups(perm.reshape(3, 4).tolist())
+        ja, jb = rng.choice(3, size=2, replace=False)
+        d = int(rng.choice(p.groups[ja]))
+        d2 = int(rng.choice(p.groups[jb]))
+        cut = lambda ga, gb: sum(wm[x, y] for x in ga for y in gb)
+        before = cut(p.groups[ja], p.groups[jb])
+        after = cut([x for x in p.groups[ja] if x != d] + [d2], [x for x in p.groups[jb] if x != d2] + [d])
+        assert S.gain_kl(sw, p, d, d2) == before - after
+
+
+def test_passes_match_golden():
+    for c in I.fixture("search.json")["passes"]:
+        if not _gpu_ok(c["inst"]):
+            continue
+        g, w = I.instance(c["inst"])
+        rng = np.random.Generator(np.random.PCG64(c["seed"]))
+        ch, out = S.refine_pass(g, w, hs.Partition.from_groups(c["groups"]), c["kind"], rng, c["phase"])
+        assert ch == c["changed"], (c["inst"], c["kind"], c["phase"])
+        assert [list(x) for x in out.groups] == [sorted(x) for x in c["out"]], (c["inst"], c["kind"], c["phase"])
+        assert _rng_tuple(rng) == c["rng_after"]
+
+
+def test_crossover_matches_golden():
+    for c in I.fixture("search.json")["crossover"]:
+        rng = np.random.Generator(np.random.PCG64(c["seed"]))
+        child = S.crossover(hs.Partition.from_groups(c["p1"]), hs.Partition.from_groups(c["p2"]), rng)
+        assert [list(x) for x in child.groups] == c["child"]
+        assert _rng_tuple(rng) == c["rng_after"]
+
+
+def test_crossover_identical_parents_is_copy_and_balanced():
+    good = hs.Partition(((0, 1), (2, 3)))
+    assert S.crossover(good, good, np.random.default_rng(0)) == good
+    rng = np.random.default_rng(42)
+    for _ in range(50):
+        p1 = S.random_partition(rng, 12, 3, 4)
+        p2 = S.random_partition(rng, 12, 3, 4)
+        child = S.crossover(p1, p2, rng)
+        assert sorted(d for grp in child.groups for d in grp) == list(range(12))
+
+
+def test_local_search_matches_golden():
+    for c in I.fixture("search.json")["local_search"]:
+        if not _gpu_ok(c["inst"]):
+            continue
+        g, w = I.instance(c["inst"])
+        rng = np.random.default_rng(c["seed"])
+        out = S.local_search(g, w, hs.Partition.from_groups(c["groups"]), kind=c["kind"], rng=rng)
+        assert [list(x) for x in out.groups] == c["out"], (c["inst"], c["kind"])
+        assert _rng_tuple(rng) == c["rng_after"]
+
+
+def test_init_population_matches_numpy_draws():
+    g, w = I.instance("case5")
+    cfg = S.ScheduleConfig(pop_size=16, seed=3)
+    pop = S.init_population(g, w, cfg)
+    rng = np.random.Generator(np.random.PCG64(3))
+    for p in pop:
+        perm = rng.permutation(64)
+        assert [list(x) for x in p.groups] == [sorted(perm[j * 8:(j + 1) * 8].tolist()) for j in range(8)]
+
+
+def _check_result(res, run):
+    d = res.to_dict()
+    assert d["partition"] == run["partition"]
+    assert d["cost"]["total"] == fx(run["total"])
+    assert d["cost"]["datap"] == fx(run["datap"]) and d["cost"]["pipelinep"] == fx(run["pipelinep"])
+    assert d["cost"]["per_group_datap"] == [fx(x) for x in run["per_group"]]
+    assert d["cost"]["pipeline_order"] == run["order"]
+    assert d["evaluations"] == run["evaluations"]
+    assert [r[1] for r in d["trace"]] == [fx(x) for x in run["trace_best"]]
+    assert [r[2] for r in d["trace"]] == [fx(x) for x in run["trace_mean"]]
+
+
+@pytest.mark.parametrize("idx", range(len(I.fixture("evolve.json")["runs"])))
+def test_evolve_matches_reference_golden(idx):
+    run = I.fixture("evolve.json")["runs"][idx]
+    if not _gpu_ok(run["inst"]):
+        pytest.skip("shape beyond the GPU GA")
+    g, w = I.instance(run["inst"])
+    cfg = S.ScheduleConfig(pop_size=run["pop"], generations=run["gens"], local_search=run["kind"], seed=run["seed"],
+                           patience=run["patience"])
+    _check_result(S.evolve(g, w, cfg), run)
+
+
+@pytest.mark.parametrize("idx", range(len(I.fixture("evolve_1000.json")["runs"])))
+def test_evolve_1000_generations_matches_reference(idx):
+    """GA time-to-converge anchors: identical trace, partition, evaluations."""
+    run = I.fixture("evolve_1000.json")["runs"][idx]
+    g, w = I.instance(run["inst"])
+    cfg = S.ScheduleConfig(pop_size=run["pop"], generations=run["gens"], local_search=run["kind"], seed=run["seed"])
+    _check_result(S.evolve(g, w, cfg), run)
+
+
+@pytest.mark.parametrize("case", [1, 3, 4, 5])
+def test_islands_equal_independent_runs_vs_oracle(case):
+    """48 islands in one launch == 48 oracle evolve runs with the same streams."""
+    g, w = I.instance(f"case{case}")
+    cfg = S.ScheduleConfig(pop_size=16, generations=30, local_search="ours" if case % 2 else "kl")
+    rngs = S.island_seeds(case, 48)
+    states = [O.PCG64State.from_generator(r) for r in S.island_seeds(case, 48)]
+    sess = S.GASession(g, w, cfg, rngs)
+    sess.run(cfg.generations)
+    res = sess.results()
+    orc = O.Oracle.of(g, w)
+    for i, r in enumerate(res):
+        o = orc.evolve(cfg.pop_size, cfg.generations, cfg.local_search, state=states[i])
+        assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+        assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+        assert [t[1] for t in r.trace] == list(o["trace_best"])
+        assert [t[2] for t in r.trace] == list(o["trace_mean"])
+        assert O.PCG64State.from_generator(rngs[i]).as_tuple() == states[i].as_tuple()
+
+
+def test_epochs_equal_single_launch():
+    g, w = I.instance("case5")
+    cfg = S.ScheduleConfig(pop_size=32, generations=40, local_search="ours", seed=9)
+    one = S.evolve(g, w, cfg)
+    sess = S.GASession(g, w, cfg, [np.random.Generator(np.random.PCG64(9))])
+    for until in (7, 19, 33, 40):
+        sess.run(until)
+    assert sess.results()[0].to_dict() == one.to_dict()
+
+
+def test_migration_is_deterministic_and_keeps_best_monotone():
+    g, w = I.instance("case5")
+    cfg = S.ScheduleConfig(pop_size=16, generations=30, local_search="kl")
+
+    def run():
+        sess = S.GASession(g, w, cfg, S.island_seeds(1, 8))
+        for epoch in range(3):
+            sess.run(10 * (epoch + 1))
+            gr, co = sess.export_elites(2)
+            sess.import_elites(gr, co, [(i - 1) % 8 for i in range(8)])
+        return sess.results()
+
+    a, b = run(), run()
+    assert [r.to_dict() for r in a] == [r.to_dict() for r in b]
+    for r in a:
+        best = [t[1] for t in r.trace]
+        assert all(y <= x for x, y in zip(best, best[1:]))
+        assert r.best_cost.total == hs.comm_cost(g, r.best_partition, w).total
+
+
+def test_evolve_errors_like_reference():
+    g, w = I.instance("r4_1x4")
+    with pytest.raises(ValueError):
+        S.evolve(g, w, S.ScheduleConfig(pop_size=4, generations=3, local_search="ours"))
+    res = S.evolve(g, w, S.ScheduleConfig(pop_size=4, generations=3, local_search="kl"))
+    assert res.best_cost.pipelinep == 0.0
