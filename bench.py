@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--case", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ga", action="store_true", help="skip the GA time-to-converge / island legs")
+    ap.add_argument("--islands", type=int, default=0, help="GA islands per GPU (default: one per SM)")
+    ap.add_argument("--island-gens", type=int, default=100)
     return ap.parse_args()
 
 
@@ -69,6 +72,10 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:  # sampler is live before timing starts
+                time.sleep(0.02)
+            self.skip = len(self.lines)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -87,7 +94,7 @@ class ClockSampler:
 
     def summary(self):
         rows = []
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "skip", 0):] or self.lines[-1:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -270,6 +277,8 @@ def run_ours():
         "gpu_launches": ARGS.steps,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }
+    if not ARGS.no_ga:
+        line["ga"] = ga_legs(g, w, rank, world, local, barrier, dist)
     if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
         from oracle import oracle as O
         threads = O.cpu_count()
@@ -281,6 +290,56 @@ def run_ours():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def ga_legs(g, w, rank, world, local, barrier, dist):
+    """GA time-to-converge (the reference's 1000-generation case-5 run, one
+    seed, latency) and island throughput (one GA per SM, elite migration over
+    NCCL every 25 generations)."""
+    import torch
+    from paper_2206_01288_b200 import scheduler as S
+
+    out = {}
+    cfg = S.ScheduleConfig(pop_size=64, generations=1000, local_search="ours", seed=0)
+    barrier()
+    t0 = time.perf_counter()
+    res = S.evolve(g, w, cfg)
+    torch.cuda.synchronize()
+    t_ga = time.perf_counter() - t0
+    best = [b for _, b, _ in res.trace]
+    conv = max([0] + [i for i in range(1, len(best)) if best[i] < best[i - 1]])
+    gold_path = ROOT / "tests" / "golden" / "evolve_1000.json"
+    ident, ref_s = None, None
+    if gold_path.exists() and ARGS.case == 5:
+        run = next(r for r in json.loads(gold_path.read_text())["runs"] if r["inst"] == "case5")
+        ref_s = run["wall_s"]
+        ident = (res.evaluations == run["evaluations"]
+                 and [b for _, b, _ in res.trace] == [float.fromhex(x) for x in run["trace_best"]]
+                 and [m for _, _, m in res.trace] == [float.fromhex(x) for x in run["trace_mean"]]
+                 and [list(x) for x in res.best_partition.key()] == run["partition"])
+    out["time_to_converge"] = {
+        "workload": f"evolve(pop=64, generations=1000, local_search='ours', seed=0), case {ARGS.case}",
+        "seconds": t_ga, "generations": len(res.trace), "last_improving_generation": conv,
+        "best_total_s": res.best_cost.total, "evaluations": res.evaluations,
+        "identical_to_reference": ident,
+        "reference_python_seconds_build_container": ref_s,
+    }
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    I = ARGS.islands or sms
+    icfg = S.ScheduleConfig(pop_size=64, generations=ARGS.island_gens, local_search="ours", seed=1)
+    barrier()
+    t0 = time.perf_counter()
+    S.evolve_islands(g, w, icfg, I, migrate_every=25, elites=2)
+    torch.cuda.synchronize()
+    barrier()
+    tt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_isl = float(tt.item())
+    out["islands"] = {"islands": I * world, "generations": ARGS.island_gens, "seconds": t_isl,
+                      "island_generations_per_s": I * world * ARGS.island_gens / t_isl,
+                      "migration": "2 elites every 25 generations, global ring, NCCL all-gather"}
+    return out
 
 
 if __name__ == "__main__":

@@ -342,3 +342,56 @@ def island_seeds(seed: int, islands: int, offset: int = 0) -> list[np.random.Gen
     convention of evaluation.py:295-298."""
     children = np.random.SeedSequence(seed).spawn(offset + islands)[offset:]
     return [np.random.Generator(np.random.PCG64(c)) for c in children]
+
+
+# ---------------------------------------------------------------------------
+# island model across GPUs (new capability, SURVEY.md §8e)
+
+def migration_sources(rank: int, world: int, islands_per_rank: int) -> list[int]:
+    """Ring over global island ids: island r*I+i receives from r*I+i-1."""
+    total = world * islands_per_rank
+    return [(rank * islands_per_rank + i - 1) % total for i in range(islands_per_rank)]
+
+
+def gather_elites(groups, costs, group=None):
+    """All-gather [I, E, k*m] int16 layouts and [I, E] f64 costs over the
+    default process group (NCCL on GPUs, gloo on CPU); identity if
+    torch.distributed is not initialized.  int16 travels as bytes."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return groups, costs
+    world = dist.get_world_size(group)
+    gb = groups.contiguous().view(torch.uint8)
+    gl = [torch.empty_like(gb) for _ in range(world)]
+    cl = [torch.empty_like(costs) for _ in range(world)]
+    dist.all_gather(gl, gb, group=group)
+    dist.all_gather(cl, costs.contiguous(), group=group)
+    return torch.cat(gl).view(torch.int16).view(-1, *groups.shape[1:]), torch.cat(cl)
+
+
+def evolve_islands(g, w, cfg: ScheduleConfig, islands_per_rank: int, migrate_every: int = 0, elites: int = 2,
+                   group=None) -> list[ScheduleResult]:
+    """Run islands_per_rank GA instances on this rank's GPU, streams from
+    SeedSequence(cfg.seed).spawn(world * islands_per_rank); every
+    `migrate_every` generations (0 = never) each island sends its `elites`
+    best members to the next island of a global ring (NCCL all-gather)."""
+    import torch.distributed as dist
+    dist_on = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if dist_on else 0
+    world = dist.get_world_size(group) if dist_on else 1
+    I = int(islands_per_rank)
+    rngs = island_seeds(cfg.seed, I, offset=rank * I)
+    sess = GASession(g, w, cfg, rngs)
+    src = migration_sources(rank, world, I)
+    gen = 0
+    while gen < cfg.generations:
+        nxt = cfg.generations if migrate_every <= 0 else min(cfg.generations, gen + migrate_every)
+        sess.run(nxt)
+        gen = nxt
+        if migrate_every > 0 and gen < cfg.generations:
+            gr, co = sess.export_elites(elites)
+            all_gr, all_co = gather_elites(gr, co, group)
+            sess.import_elites(all_gr, all_co, src)
+    seeds = [cfg.seed] * I
+    return sess.results(seeds)
