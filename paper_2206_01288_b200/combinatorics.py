@@ -16,7 +16,7 @@ import numpy as np
 from . import _native as N
 
 MAX_EXACT_TSP = 16
-MAX_GPU_PATH_K = 8
+MAX_GPU_PATH_K = 16
 MAX_GPU_MATCH_M = 64
 
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/hetsched_b200.h"
+#include "hs_big.h"
 #include "hs_eval.cuh"
 #include "hs_instance.h"
 
@@ -93,10 +94,60 @@ int get_hk(int device, int k, hs::HKTables* out) {
     return 0;
 }
 
+// 9 <= k <= 16: same layout as hk_schedule with 64-bit words
+struct DeviceHKBig {
+    uint64_t* st = nullptr;
+    uint32_t* off = nullptr;
+    hs::HKBig t{};
+};
+std::map<std::pair<int, int>, DeviceHKBig> g_hkb;
+
+int get_hk_big(int device, int k, hs::HKBig* out) {
+    std::lock_guard<std::mutex> lk(g_hk_mu);
+    auto key = std::make_pair(device, k);
+    auto it = g_hkb.find(key);
+    if (it == g_hkb.end()) {
+        DeviceHKBig d;
+        std::vector<uint32_t> off((size_t)1 << k, 0);
+        uint32_t acc = 0;
+        for (int s = 0; s < (1 << k); s++) {
+            off[s] = acc;
+            if (__builtin_popcount(s) >= 2) acc += __builtin_popcount(s);
+        }
+        std::vector<uint64_t> st;
+        for (int p = 0; p < 18; p++) {
+            d.t.lay[p] = (int)st.size();
+            if (p < 2 || p > k) continue;
+            for (int r = 0; r < (1 << k); r++) {
+                if (__builtin_popcount(r) != p - 1) continue;
+                for (int u = 0; u < k; u++) {
+                    if (r >> u & 1) continue;
+                    int s = r | (1 << u);
+                    uint64_t dst = off[s] + __builtin_popcount(s & ((1 << u) - 1));
+                    uint64_t offr = __builtin_popcount(r) >= 2 ? off[r] : 0;
+                    st.push_back(offr | (dst << 20) | ((uint64_t)u << 40) | ((uint64_t)r << 44));
+                }
+            }
+        }
+        CK(cudaMalloc(&d.st, std::max<size_t>(8, st.size() * 8)), "cudaMalloc hkb");
+        CK(cudaMalloc(&d.off, off.size() * 4), "cudaMalloc hkb");
+        if (!st.empty()) CK(cudaMemcpy(d.st, st.data(), st.size() * 8, cudaMemcpyHostToDevice), "upload hkb");
+        CK(cudaMemcpy(d.off, off.data(), off.size() * 4, cudaMemcpyHostToDevice), "upload hkb");
+        d.t.states = d.st;
+        d.t.nstates = (int)st.size();
+        d.t.off = d.off;
+        d.t.noff = (int)off.size();
+        it = g_hkb.emplace(key, d).first;
+    }
+    *out = it->second.t;
+    return 0;
+}
+
 }  // namespace hsx
 
 using hsx::fail;
 using hsx::get_hk;
+using hsx::get_hk_big;
 using hsx::DeviceGuard;
 using hsx::g_err;
 
@@ -114,6 +165,13 @@ static hs::EvalArgs base_args(const hs_instance* h) {
     return a;
 }
 
+static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
+    if (h->k > hs::kWarpK)
+        return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
+                                   a.key16 && a.m == 8 && a.nvals <= 0x8000, s);
+    return hs::launch_eval(a, h->plan, s);
+}
+
 extern "C" {
 
 int hs_version(void) { return 1; }
@@ -125,7 +183,7 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
     if (!out || !lat || !bw) return fail(-2, "null argument");
     if (n < 1 || d_pp < 1 || d_dp < 1 || (int64_t)d_pp * d_dp != n) return fail(-2, "d_pp*d_dp must equal n");
     if (d_dp > hs::kMaxM) return fail(-3, "d_dp > 64 is not supported");
-    if (d_pp > hs::kWarpK) return fail(-3, "d_pp > 8 is not supported by the warp evaluator yet");
+    if (d_pp > 16) return fail(-3, "d_pp > 16 needs the heuristic path search (exact Held-Karp is limited to 16)");
     if (n > 32767) return fail(-3, "n > 32767 is not supported (int16 device ids)");
     DeviceGuard dg(device);
     hs_instance* h = new hs_instance();
@@ -165,10 +223,18 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
         if (hs::launch_narrow((int64_t)nn, h->rank, h->rank16, 0)) return fail(-1, "narrow launch");
     }
     CK(cudaDeviceSynchronize(), "instance tables");
-    int rc = get_hk(device, d_pp, &h->hk);
+    int rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk);
     if (rc) return rc;
-    hs::EvalArgs a = base_args(h);
-    if (hs::eval_plan(a, h->sm_count, h->smem_optin, &h->plan)) return fail(-3, "shape does not fit shared memory");
+    if (d_pp > hs::kWarpK) {
+        rc = get_hk_big(device, d_pp, &h->hkb);
+        if (rc) return rc;
+        h->big_blocks = hs::big_blocks(h->sm_count, d_pp);
+        for (int i = 0; i < 2; i++)
+            CK(cudaMalloc(&h->big_scratch[i], (size_t)h->big_blocks * hs::hk_big_size(d_pp) * 8), "cudaMalloc scratch");
+    } else {
+        hs::EvalArgs a = base_args(h);
+        if (hs::eval_plan(a, h->sm_count, h->smem_optin, &h->plan)) return fail(-3, "shape does not fit shared memory");
+    }
     *out = h;
     return 0;
 }
@@ -184,6 +250,8 @@ int hs_instance_destroy(hs_instance* h) {
     cudaFree(h->vals);
     cudaFree(h->rank);
     if (h->rank16) cudaFree(h->rank16);
+    for (int i = 0; i < 2; i++)
+        if (h->big_scratch[i]) cudaFree(h->big_scratch[i]);
     cudaFree(h->invalid);
     for (int i = 0; i < 2; i++) {
         if (h->cg[i]) cudaFree(h->cg[i]);
@@ -221,7 +289,7 @@ int hs_eval_batch(hs_instance* h, const int16_t* groups, int64_t P, double* tota
     a.per_group = per_group;
     a.order = order;
     a.invalid = invalid ? invalid : h->invalid;
-    if (hs::launch_eval(a, h->plan, (cudaStream_t)stream)) return fail(-1, "eval launch", cudaGetLastError());
+    if (launch_any(h, a, 0, (cudaStream_t)stream)) return fail(-1, "eval launch", cudaGetLastError());
     return 0;
 }
 
@@ -260,7 +328,7 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
         a.pipe = h->co[b] + 2 * h->chunk;
         a.per_group = per_group ? h->co[b] + 3 * h->chunk : nullptr;
         a.order = order ? reinterpret_cast<int8_t*>(h->co[b] + (3 + h->k) * h->chunk) : nullptr;
-        if (hs::launch_eval(a, h->plan, s)) return fail(-1, "eval launch", cudaGetLastError());
+        if (launch_any(h, a, b, s)) return fail(-1, "eval launch", cudaGetLastError());
         CK(cudaMemcpyAsync(total + lo, a.total, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
         if (datap) CK(cudaMemcpyAsync(datap + lo, a.datap, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
         if (pipelinep) CK(cudaMemcpyAsync(pipelinep + lo, a.pipe, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
@@ -284,7 +352,7 @@ int hs_bottleneck_batch(const double* w, int m, int64_t B, double* out, int devi
 }
 
 int hs_path_batch(const double* w, int k, int64_t B, double* total, int8_t* order, int device, void* stream) {
-    if (k < 1 || k > hs::kWarpK) return fail(-3, "path: k must be in 1..8");
+    if (k < 1 || k > 16) return fail(-3, "path: k must be in 1..16");
     DeviceGuard dg(device);
     if (k == 1) {
         // a single vertex: empty path (combinatorics.py:241-242)
@@ -295,11 +363,24 @@ int hs_path_batch(const double* w, int k, int64_t B, double* total, int8_t* orde
         CK(cudaStreamSynchronize((cudaStream_t)stream), "sync");
         return 0;
     }
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device), "props");
+    if (k > hs::kWarpK) {
+        hs::HKBig t;
+        int rc = get_hk_big(device, k, &t);
+        if (rc) return rc;
+        int blocks = (int)std::min<int64_t>(B, hs::big_blocks(prop.multiProcessorCount, k));
+        double* scratch = nullptr;
+        CK(cudaMalloc(&scratch, (size_t)std::max(blocks, 1) * hs::hk_big_size(k) * 8), "cudaMalloc scratch");
+        int lrc = hs::launch_path_cta(w, k, B, t, scratch, blocks, total, order, (cudaStream_t)stream);
+        cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+        cudaFree(scratch);
+        if (lrc || e != cudaSuccess) return fail(-1, "path launch", e);
+        return 0;
+    }
     hs::HKTables t;
     int rc = get_hk(device, k, &t);
     if (rc) return rc;
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device), "props");
     if (hs::launch_path_batch(w, k, B, t, total, order, prop.multiProcessorCount, (cudaStream_t)stream))
         return fail(-1, "path launch", cudaGetLastError());
     return 0;

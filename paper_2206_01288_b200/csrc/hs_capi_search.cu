@@ -39,6 +39,7 @@ int check_search_shape(const hs_instance* h, int kind, int max_passes) {
     if (kind == 0 && h->k == 1 && h->m >= 2)
         return fail(-4, "zero-size array to reduction operation maximum which has no identity");
     if (h->n > 1024) return fail(-3, "search kernels support n <= 1024");
+    if (h->k > 8) return fail(-3, "the device GA / local search currently cover d_pp <= 8");
     return 0;
 }
 

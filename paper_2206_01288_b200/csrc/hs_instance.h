@@ -11,6 +11,7 @@ namespace hsx {
 
 int fail(int code, const char* what, cudaError_t e = cudaSuccess);
 int get_hk(int device, int k, hs::HKTables* out);
+int get_hk_big(int device, int k, hs::HKBig* out);
 
 struct DeviceGuard {
     int prev = -1;
@@ -41,6 +42,9 @@ struct hs_instance {
     uint16_t* rank16 = nullptr;
     int nvals = 0;
     hs::HKTables hk{};
+    hs::HKBig hkb{};               // d_pp > 8: CTA evaluator schedule
+    double* big_scratch[2] = {nullptr, nullptr};  // per-CTA Held-Karp slices (two stream sets)
+    int big_blocks = 0;
     int* invalid = nullptr;
     hs::EvalPlan plan{};
     // host-buffer path

@@ -15,6 +15,17 @@ struct HKTables {
     int nhoff;
 };
 
+// Held-Karp schedule for 9 <= k <= 16 (one CTA per candidate): 64-bit state
+// words off[r] (20) | dst (20) | u (4) | r (16) grouped by layer, and the
+// compact offsets off[s] (2^k entries).
+struct HKBig {
+    const uint64_t* states;
+    int nstates;
+    int lay[18];
+    const uint32_t* off;
+    int noff;
+};
+
 struct EvalArgs {
     int n, k, m;
     const double* dp;    // n*n data-parallel pair seconds (0 diagonal)

@@ -159,6 +159,12 @@ def config1_scenario() -> Scenario:
     return scenario_from_ms_gbps([(4, 0.1, 100)] * 2, 0.25, 25, seed=0, name="config1")
 
 
+def config4_scenario(seed: int = 0) -> Scenario:
+    """BASELINE config 4: 512 devices as 16 world-wide regions of 32 with the
+    case-5 link ranges."""
+    return Scenario("config4", (Region(32, 0.005, 2e9),) * 16, (0.010, 0.250), (0.3e9, 1.3e9), seed)
+
+
 def random_graph(seed: int, n: int, lat_range=(0.001, 0.05), bw_range=(1e9, 1e10)) -> CommGraph:
     """Seeded heterogeneous clique (reference tests/conftest.py:50-60 recipe:
     default_rng(seed), lat drawn before bw)."""

@@ -13,7 +13,8 @@ from pathlib import Path
 
 import numpy as np
 
-from paper_2206_01288_b200.netmodel import CommGraph, random_graph, scenario_case, scenario_from_ms_gbps
+from paper_2206_01288_b200.netmodel import (CommGraph, config4_scenario, random_graph, scenario_case,
+                                            scenario_from_ms_gbps)
 from paper_2206_01288_b200.workload import WorkloadSpec
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
@@ -50,6 +51,8 @@ def build(recipe: dict):
         g = scenario_from_ms_gbps(regs, sp["cross"]["delay_ms"], sp["cross"]["bw_gbps"], sp.get("seed", 0)).graph()
     elif kind == "random":
         g = random_graph(recipe["seed"], recipe["n"])
+    elif kind == "config4":
+        g = config4_scenario().graph()
     else:
         raise ValueError(kind)
     return g, WorkloadSpec(*recipe["w"])

@@ -78,6 +78,10 @@ def instance(recipe: dict):
         g = H.symmetrize(H.generate_scenario(spec_from_dict(recipe["spec"])))
     elif kind == "random":
         g = make_random_graph(np.random.default_rng(recipe["seed"]), recipe["n"])
+    elif kind == "config4":
+        spec = H.ScenarioSpec("config4", tuple(H.netmodel.GroupSpec(32, 0.005, 2e9, f"r{i}") for i in range(16)),
+                              (0.010, 0.250), (0.3e9, 1.3e9), 0)
+        g = H.symmetrize(H.generate_scenario(spec))
     else:
         raise ValueError(kind)
     w = H.WorkloadSpec(*recipe["w"])
@@ -109,6 +113,11 @@ INSTANCES = {
     "r10_10x1": {"kind": "random", "seed": 25, "n": 10, "w": [10, 1, 1e9, 3e8]},
     "r4_1x4": {"kind": "random", "seed": 26, "n": 4, "w": [1, 4, 1e9, 3e8]},
     "r64_2x32": {"kind": "random", "seed": 27, "n": 64, "w": [2, 32, 1e9, 3e8]},
+    "r32_16x2": {"kind": "random", "seed": 28, "n": 32, "w": [16, 2, 1e9, 3e8]},
+    "r48_12x4": {"kind": "random", "seed": 29, "n": 48, "w": [12, 4, 1e9, 3e8]},
+    "r128_16x8": {"kind": "random", "seed": 30, "n": 128, "w": [16, 8, 1_073_741_824, 301_989_888]},
+    "config4": {"kind": "config4", "w": [16, 32, 268_435_456, 201_326_592]},
+    "config5": {"kind": "random", "seed": 0, "n": 1024, "w": [16, 64, 268_435_456, 201_326_592]},
 }
 
 
@@ -127,6 +136,8 @@ def gen_costs():
     for name, rec in INSTANCES.items():
         g, w = instance(rec)
         count = 400 if g.n == 64 and name.startswith("case") else 120
+        if w.d_pp >= 12:
+            count = 4 if g.n >= 512 else 12
         if name == "g4":
             parts = np.array([[[0, 1], [2, 3]], [[0, 2], [1, 3]], [[0, 3], [1, 2]]], dtype=np.int16)
         else:

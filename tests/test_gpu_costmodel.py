@@ -17,7 +17,7 @@ hs = pytest.importorskip("paper_2206_01288_b200")
 
 
 def _gpu_names():
-    return [n for n, m in I.meta().items() if m["recipe"]["w"][0] <= 8 and m["recipe"]["w"][1] <= 64]
+    return [n for n, m in I.meta().items() if m["recipe"]["w"][0] <= 16 and m["recipe"]["w"][1] <= 64]
 
 
 @pytest.mark.parametrize("name", sorted(_gpu_names()))
@@ -153,8 +153,6 @@ def test_bottleneck_and_path_solvers_vs_golden():
         assert hs.bottleneck_value(wm) == I.fx(c["value"])
     for c in fxs["tsp"]:
         k = c["k"]
-        if k > 8:
-            continue
         wm = np.array([I.fx(x) for x in c["w"]]).reshape(k, k)
         r = hs.open_loop_tsp(wm)
         assert r.total == I.fx(c["total"]) and list(r.order) == c["order"]
@@ -167,3 +165,31 @@ def test_batched_bottleneck_vs_oracle_with_ties():
         got = hs.bottleneck_values(stack)
         want = np.array([O.bottleneck_value(x) for x in stack])
         assert np.array_equal(got, want), m
+
+
+@pytest.mark.parametrize("name,count", [("r32_16x2", 300), ("r48_12x4", 200), ("r128_16x8", 100), ("config4", 12),
+                                        ("r18_9x2", 300)])
+def test_cta_path_d_pp_above_8_vs_oracle(name, count):
+    """d_pp 9..16 (one CTA per candidate, global Held-Karp scratch) vs the oracle."""
+    g, w = I.instance(name)
+    parts = _random_parts(31, count, g.n, w.d_pp, w.d_dp)
+    r = hs.comm_cost_batch(g, parts, w, per_group=True, order=True)
+    orc = O.Oracle.of(g, w)
+    t, d, p = orc.comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"], t) and np.array_equal(r["datap"], d) and np.array_equal(r["pipelinep"], p)
+    for i in range(min(count, 6)):
+        tt, dd, pp, pg, order = orc.comm_cost(parts[i])
+        assert np.array_equal(r["per_group"][i], pg) and list(r["order"][i]) == list(order)
+
+
+def test_path_solver_k_9_to_16_vs_oracle():
+    rng = np.random.default_rng(5)
+    for k in (9, 12, 14, 16):
+        stack = rng.uniform(0, 10, size=(6, k, k))
+        stack = (stack + stack.transpose(0, 2, 1)) / 2.0
+        for x in stack:
+            np.fill_diagonal(x, 0.0)
+        tot, order = hs.open_loop_tsps(stack)
+        for i in range(len(stack)):
+            o, t = O.open_loop_tsp(stack[i])
+            assert tot[i] == t and tuple(order[i]) == o
