@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "hs_big.h"
 #include "hs_instance.h"
 #include "hs_search.h"
 
@@ -39,7 +40,7 @@ int check_search_shape(const hs_instance* h, int kind, int max_passes) {
     if (kind == 0 && h->k == 1 && h->m >= 2)
         return fail(-4, "zero-size array to reduction operation maximum which has no identity");
     if (h->n > 1024) return fail(-3, "search kernels support n <= 1024");
-    if (h->k > 8) return fail(-3, "the device GA / local search currently cover d_pp <= 8");
+    if (h->k > 16) return fail(-3, "the device GA / local search cover d_pp <= 16");
     return 0;
 }
 
@@ -60,6 +61,7 @@ struct hs_ga {
     double* out_pg = nullptr;
     int8_t* out_order = nullptr;
     int16_t* out_groups = nullptr;
+    double* hk_scratch = nullptr;
 };
 
 static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
@@ -90,6 +92,9 @@ static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
     a.out_pg = ga->out_pg;
     a.out_order = ga->out_order;
     a.out_groups = ga->out_groups;
+    a.hkb = h->hkb;
+    a.hk_scratch = ga->hk_scratch;
+    a.hk_size = h->k > 8 ? hs::hk_big_size(h->k) : 0;
     return a;
 }
 
@@ -128,6 +133,7 @@ int hs_ga_create(hs_instance* h, const hs_ga_config* cfg, int islands, const hs_
     CK(cudaMalloc(&ga->out_pg, (size_t)islands * h->k * 8), "cudaMalloc");
     CK(cudaMalloc(&ga->out_order, (size_t)islands * h->k), "cudaMalloc");
     CK(cudaMalloc(&ga->out_groups, (size_t)islands * km * 2), "cudaMalloc");
+    if (h->k > 8) CK(cudaMalloc(&ga->hk_scratch, (size_t)islands * hs::hk_big_size(h->k) * 8), "cudaMalloc");
     CK(cudaMemcpy(ga->state, st.data(), sizeof(hs::GAState) * islands, cudaMemcpyHostToDevice), "upload state");
     *out = ga;
     return 0;
@@ -198,7 +204,7 @@ int hs_ga_destroy(hs_ga* ga) {
     DeviceGuard dg(ga->h->device);
     for (void* p : {(void*)ga->state, (void*)ga->pop, (void*)ga->cost, (void*)ga->best, (void*)ga->trace_best,
                     (void*)ga->trace_mean, (void*)ga->out3, (void*)ga->out_pg, (void*)ga->out_order,
-                    (void*)ga->out_groups})
+                    (void*)ga->out_groups, (void*)ga->hk_scratch})
         if (p) cudaFree(p);
     delete ga;
     return 0;
@@ -221,6 +227,8 @@ static int refine_common(hs_instance* h, int kind, int max_passes, int single, i
     DevBuf<hs_pcg64> drng;
     DevBuf<double> dcost;
     DevBuf<int> dev, dch;
+    DevBuf<double> hks;
+    if (h->k > 8) CK(hks.alloc((size_t)B * hs::hk_big_size(h->k)), "cudaMalloc");
     CK(dg_in.alloc((size_t)B * km), "cudaMalloc");
     CK(dg_out.alloc((size_t)B * km), "cudaMalloc");
     CK(drng.alloc(B), "cudaMalloc");
@@ -248,6 +256,9 @@ static int refine_common(hs_instance* h, int kind, int max_passes, int single, i
     a.out_cost = dcost.p;
     a.evaluations = dev.p;
     a.changed = dch.p;
+    a.hkb = h->hkb;
+    a.hk_scratch = hks.p;
+    a.hk_size = h->k > 8 ? hs::hk_big_size(h->k) : 0;
     if (hs::launch_refine(a, plan, B, h->rank16 != nullptr, 0)) return fail(-1, "refine launch", cudaGetLastError());
     CK(cudaDeviceSynchronize(), "refine");
     CK(cudaMemcpy(out, dg_out.p, (size_t)B * km * 2, cudaMemcpyDeviceToHost), "D2H");

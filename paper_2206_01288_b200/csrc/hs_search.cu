@@ -17,6 +17,7 @@
 
 #include "hs_rng.cuh"
 #include "hs_search.h"
+#include "hs_cta_eval.cuh"
 #include "hs_warp_eval.cuh"
 
 namespace hs {
@@ -553,29 +554,103 @@ __device__ __forceinline__ void copy16(int16_t* d, const int16_t* s, int n, int 
     for (int t = lane; t < n; t += kWarp) d[t] = s[t];
 }
 
-// Prices candidates cand[0..cnt) (smem, km each) round-robin over the CTA's
-// warps; cost[i] = datap + pipelinep.
-template <typename KeyT, bool kM8>
-__device__ __noinline__ void price_all(const EvalView<KeyT>& v, const WarpScratch& ws, const int16_t* cand,
-                                          int cnt, int km, double* cost, int wid, int W, int lane) {
-    for (int i = wid; i < cnt; i += W) {
-        double dp, pp;
-        warp_price<KeyT, kM8>(v, ws, cand + (size_t)i * km, lane, dp, pp);
-        if (lane == 0) cost[i] = dp + pp;
-        __syncwarp();
+// Prices candidates cand[0..cnt) (smem, km each): round-robin over the CTA's
+// warps (d_pp <= 8, K1 warp evaluator) or one after another with the whole
+// CTA (d_pp 9..16, hs_cta_eval.cuh); cost[i] = datap + pipelinep.  Called by
+// every thread of the CTA.
+template <typename KeyT, bool kM8, bool kCta>
+struct Pricer {
+    EvalView<KeyT> v;
+    WarpScratch ws;
+    CtaScratch cs;
+    HKBig hkb;
+    double* h;
+
+    __device__ __noinline__ void all(const int16_t* cand, int cnt, int km, double* cost, int wid, int W,
+                                     int lane) const {
+        if constexpr (kCta) {
+            for (int i = 0; i < cnt; i++) {
+                double dp, pp;
+                cta_price<KeyT, kM8>(v.n, v.k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand + (size_t)i * km, dp, pp);
+                if (threadIdx.x == 0) cost[i] = dp + pp;
+                __syncthreads();
+            }
+        } else {
+            for (int i = wid; i < cnt; i += W) {
+                double dp, pp;
+                warp_price<KeyT, kM8>(v, ws, cand + (size_t)i * km, lane, dp, pp);
+                if (lane == 0) cost[i] = dp + pp;
+                __syncwarp();
+            }
+        }
     }
+
+    // price one candidate with full outputs; every thread calls it
+    __device__ void one(const int16_t* cand, int wid, int lane, double* out3, double* out_pg, int8_t* out_order) const {
+        const int k = v.k;
+        if constexpr (kCta) {
+            double dp, pp;
+            cta_price<KeyT, kM8>(v.n, k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand, dp, pp);
+            if (threadIdx.x == 0) {
+                out3[0] = dp + pp;
+                out3[1] = dp;
+                out3[2] = pp;
+                if (out_order) held_karp_order_big(k, cs.E, h, hkb.off, pp, out_order);
+            }
+            if (out_pg && threadIdx.x < k) out_pg[threadIdx.x] = cs.pg[threadIdx.x];
+            __syncthreads();
+        } else {
+            if (wid == 0) {
+                double dp, pp;
+                warp_price<KeyT, kM8>(v, ws, cand, lane, dp, pp);
+                if (lane == 0) {
+                    out3[0] = dp + pp;
+                    out3[1] = dp;
+                    out3[2] = pp;
+                    if (out_order) held_karp_order(k, ws.E, ws.h, v.hk.hoff, pp, out_order);
+                }
+                if (out_pg && lane < k) out_pg[lane] = ws.pg[lane];
+            }
+            __syncthreads();
+        }
+    }
+};
+
+// Sets up the pricer's shared-memory pieces; advances `off`.
+template <bool kSmemTables, typename KeyT, bool kM8, bool kCta>
+__device__ inline Pricer<KeyT, kM8, kCta> make_pricer(int n, int k, int m, const double* dp, const void* rank,
+                                                      const double* vals, const HKTables& hkt, const HKBig& hkb,
+                                                      double* hk_scratch, size_t hk_size, const ScratchLayout& wl,
+                                                      unsigned char* smem, size_t& off, int wid, int W) {
+    Pricer<KeyT, kM8, kCta> pr;
+    HKSmem hk{};
+    if constexpr (!kCta) {
+        hk = hk_stage(hkt, smem);
+        off = hk_smem_bytes(hkt);
+    }
+    pr.v = stage_tables<kSmemTables, KeyT>(n, k, m, dp, rank, vals, hk, smem, off);
+    if constexpr (kCta) {
+        pr.cs = cta_scratch_at(smem + off, k, m);
+        off += (cta_scratch_bytes(k, m) + 15) & ~(size_t)15;
+        pr.hkb = hkb;
+        pr.h = hk_scratch + (size_t)blockIdx.x * hk_size;
+    } else {
+        pr.ws = scratch_at(smem + off + (size_t)wid * wl.bytes, wl);
+        off += (size_t)W * wl.bytes;
+    }
+    return pr;
 }
 
-template <bool kSmemTables, typename KeyT, bool kM8>
+template <bool kSmemTables, typename KeyT, bool kM8, bool kCta>
 __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int isl = blockIdx.x;
     const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m, P = a.pop, cap = m + 1;
     const int max_snaps = 1 + a.max_passes;
-    HKSmem hk = hk_stage(a.hk, smem);
-    size_t off = hk_smem_bytes(a.hk);
-    EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
+    size_t off = 0;
+    const Pricer<KeyT, kM8, kCta> pr = make_pricer<kSmemTables, KeyT, kM8, kCta>(
+        n, k, m, a.dp, a.rank, a.vals, a.hk, a.hkb, a.hk_scratch, a.hk_size, wl, smem, off, wid, W);
     const double* SW;
     if (kSmemTables) {
         double* ssw = reinterpret_cast<double*>(smem + off);
@@ -585,8 +660,6 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     } else {
         SW = a.sw;
     }
-    WarpScratch ws = scratch_at(smem + off + (size_t)wid * wl.bytes, wl);
-    off += (size_t)W * wl.bytes;
     auto take = [&](size_t bytes) {
         unsigned char* p = smem + off;
         off += (bytes + 15) & ~(size_t)15;
@@ -668,7 +741,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             int cnt = min(max_snaps, P - c0);
             for (int t = threadIdx.x; t < cnt * km; t += blockDim.x) g.snaps[t] = pop[(size_t)c0 * km + t];
             __syncthreads();
-            price_all<KeyT, kM8>(v, ws, g.snaps, cnt, km, g.popcost + c0, wid, W, lane);
+            pr.all(g.snaps, cnt, km, g.popcost + c0, wid, W, lane);
             __syncthreads();
         }
         if (driver) {
@@ -738,7 +811,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         }
         __syncthreads();
         const int nsnap = g.ctl[0];
-        price_all<KeyT, kM8>(v, ws, g.snaps, nsnap, km, g.snapcost, wid, W, lane);
+        pr.all(g.snaps, nsnap, km, g.snapcost, wid, W, lane);
         __syncthreads();
         if (driver) {
             int bsi = 0, worst = 0, replace = 0, improve = 0;
@@ -788,34 +861,29 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     bool finished = g.ctl[1] || g.ctl[2] >= a.generations;
     if (finished && a.finalize && !st.finalized) {
         // canonical() (costmodel.py:86-88) then a last priced evaluation (:572-574)
-        if (driver) {
-            if (lane == 0) {
-                int ord[16];
-                for (int j = 0; j < k; j++) ord[j] = j;
-                for (int x = 1; x < k; x++) {
-                    int y = ord[x], b = x - 1;
-                    while (b >= 0 && gbest[ord[b] * m] > gbest[y * m]) {
-                        ord[b + 1] = ord[b];
-                        b--;
-                    }
-                    ord[b + 1] = y;
+        if (driver && lane == 0) {
+            int ord[16];
+            for (int j = 0; j < k; j++) ord[j] = j;
+            for (int x = 1; x < k; x++) {
+                int y = ord[x], b = x - 1;
+                while (b >= 0 && gbest[ord[b] * m] > gbest[y * m]) {
+                    ord[b + 1] = ord[b];
+                    b--;
                 }
-                for (int j = 0; j < k; j++)
-                    for (int i = 0; i < m; i++) g.snaps[j * m + i] = gbest[ord[j] * m + i];
+                ord[b + 1] = y;
             }
-            __syncwarp();
-            double dp, pp;
-            warp_price<KeyT, kM8>(v, ws, g.snaps, lane, dp, pp);
+            for (int j = 0; j < k; j++)
+                for (int i = 0; i < m; i++) g.snaps[j * m + i] = gbest[ord[j] * m + i];
+        }
+        __syncthreads();
+        pr.one(g.snaps, wid, lane, a.out3 + isl * 3, a.out_pg ? a.out_pg + (size_t)isl * k : nullptr,
+               a.out_order ? a.out_order + (size_t)isl * k : nullptr);
+        if (driver) {
+            copy16(a.out_groups + (size_t)isl * km, g.snaps, km, lane);
             if (lane == 0) {
                 st.evaluations += 1;
-                a.out3[isl * 3 + 0] = dp + pp;
-                a.out3[isl * 3 + 1] = dp;
-                a.out3[isl * 3 + 2] = pp;
-                if (a.out_order) held_karp_order(k, ws.E, ws.h, hk.hoff, pp, a.out_order + (size_t)isl * k);
+                st.finalized = 1;
             }
-            if (lane < k && a.out_pg) a.out_pg[(size_t)isl * k + lane] = ws.pg[lane];
-            copy16(a.out_groups + (size_t)isl * km, g.snaps, km, lane);
-            if (lane == 0) st.finalized = 1;
         }
     }
     __syncthreads();
@@ -829,16 +897,16 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
 // local_search (scheduler.py:490-512): _refine on a batch of partitions, one
 // CTA each with its own PCG64 stream; returns the best truly-priced layout.
 
-template <bool kSmemTables, typename KeyT, bool kM8>
+template <bool kSmemTables, typename KeyT, bool kM8, bool kCta>
 __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int b = blockIdx.x;
     const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m, cap = m + 1;
     const int max_snaps = 1 + a.max_passes;
-    HKSmem hk = hk_stage(a.hk, smem);
-    size_t off = hk_smem_bytes(a.hk);
-    EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
+    size_t off = 0;
+    const Pricer<KeyT, kM8, kCta> pr = make_pricer<kSmemTables, KeyT, kM8, kCta>(
+        n, k, m, a.dp, a.rank, a.vals, a.hk, a.hkb, a.hk_scratch, a.hk_size, wl, smem, off, wid, W);
     const double* SW;
     if (kSmemTables) {
         double* ssw = reinterpret_cast<double*>(smem + off);
@@ -848,8 +916,6 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     } else {
         SW = a.sw;
     }
-    WarpScratch ws = scratch_at(smem + off + (size_t)wid * wl.bytes, wl);
-    off += (size_t)W * wl.bytes;
     auto take = [&](size_t bytes) {
         unsigned char* p = smem + off;
         off += (bytes + 15) & ~(size_t)15;
@@ -911,7 +977,7 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     __syncthreads();
     if (a.single_pass) return;
     const int nsnap = ctl[0];
-    price_all<KeyT, kM8>(v, ws, snaps, nsnap, km, snapcost, wid, W, lane);
+    pr.all(snaps, nsnap, km, snapcost, wid, W, lane);
     __syncthreads();
     if (wid == 0) {
         int bsi = 0;
@@ -1013,9 +1079,9 @@ static size_t ls_bytes(int n, int k, int m) {
 
 static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P) {
     auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
-    ScratchLayout wl = scratch_layout(sh.k, sh.m);
+    ScratchLayout wl = scratch_layout(sh.k <= 8 ? sh.k : 8, sh.m);
     int km = sh.k * sh.m, ms = 1 + sh.max_passes;
-    size_t b = hk_smem_bytes(sh.hk) + (size_t)W * wl.bytes;
+    size_t b = sh.k <= 8 ? hk_smem_bytes(sh.hk) + (size_t)W * wl.bytes : al(cta_scratch_bytes(sh.k, sh.m));
     if (smem_tables)
         b += (size_t)sh.n * sh.n * 8 + al((size_t)sh.n * sh.n * (sh.key16 ? 2 : 4)) + (size_t)sh.n * sh.n * 8;
     b += al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) + al((size_t)2 * km * 2) +
@@ -1033,6 +1099,7 @@ int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* pla
                 plan->smem_tables = st;
                 plan->smem = b;
                 plan->m8 = sh.key16 && sh.m == 8 && sh.nvals <= 0x8000;
+                plan->cta = sh.k > 8;
                 return 0;
             }
         }
@@ -1040,39 +1107,49 @@ int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* pla
     return -2;
 }
 
-template <bool S, typename KT, bool M8>
+template <bool S, typename KT, bool M8, bool CT>
 static int launch_ga_t(const GAArgs& a, const SearchPlan& plan, int islands, cudaStream_t st) {
-    ScratchLayout wl = scratch_layout(a.k, a.m);
-    cudaFuncSetAttribute(ga_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-    ga_kernel<S, KT, M8><<<islands, plan.warps * 32, plan.smem, st>>>(a, wl);
+    ScratchLayout wl = scratch_layout(a.k <= 8 ? a.k : 8, a.m);
+    cudaFuncSetAttribute(ga_kernel<S, KT, M8, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    ga_kernel<S, KT, M8, CT><<<islands, plan.warps * 32, plan.smem, st>>>(a, wl);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <bool CT>
+static int launch_ga_c(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st) {
+    if (plan.m8) return plan.smem_tables ? launch_ga_t<true, uint16_t, true, CT>(a, plan, islands, st)
+                                         : launch_ga_t<false, uint16_t, true, CT>(a, plan, islands, st);
+    if (key16) return plan.smem_tables ? launch_ga_t<true, uint16_t, false, CT>(a, plan, islands, st)
+                                       : launch_ga_t<false, uint16_t, false, CT>(a, plan, islands, st);
+    return plan.smem_tables ? launch_ga_t<true, uint32_t, false, CT>(a, plan, islands, st)
+                            : launch_ga_t<false, uint32_t, false, CT>(a, plan, islands, st);
 }
 
 int launch_ga(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st) {
-    if (plan.m8) return plan.smem_tables ? launch_ga_t<true, uint16_t, true>(a, plan, islands, st)
-                                         : launch_ga_t<false, uint16_t, true>(a, plan, islands, st);
-    if (key16) return plan.smem_tables ? launch_ga_t<true, uint16_t, false>(a, plan, islands, st)
-                                       : launch_ga_t<false, uint16_t, false>(a, plan, islands, st);
-    return plan.smem_tables ? launch_ga_t<true, uint32_t, false>(a, plan, islands, st)
-                            : launch_ga_t<false, uint32_t, false>(a, plan, islands, st);
+    return plan.cta ? launch_ga_c<true>(a, plan, islands, key16, st) : launch_ga_c<false>(a, plan, islands, key16, st);
 }
 
-template <bool S, typename KT, bool M8>
+template <bool S, typename KT, bool M8, bool CT>
 static int launch_refine_t(const RefineArgs& a, const SearchPlan& plan, int B, cudaStream_t st) {
-    ScratchLayout wl = scratch_layout(a.k, a.m);
-    cudaFuncSetAttribute(refine_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-    refine_kernel<S, KT, M8><<<B, plan.warps * 32, plan.smem, st>>>(a, wl);
+    ScratchLayout wl = scratch_layout(a.k <= 8 ? a.k : 8, a.m);
+    cudaFuncSetAttribute(refine_kernel<S, KT, M8, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    refine_kernel<S, KT, M8, CT><<<B, plan.warps * 32, plan.smem, st>>>(a, wl);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <bool CT>
+static int launch_refine_c(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st) {
+    if (plan.m8) return plan.smem_tables ? launch_refine_t<true, uint16_t, true, CT>(a, plan, B, st)
+                                         : launch_refine_t<false, uint16_t, true, CT>(a, plan, B, st);
+    if (key16) return plan.smem_tables ? launch_refine_t<true, uint16_t, false, CT>(a, plan, B, st)
+                                       : launch_refine_t<false, uint16_t, false, CT>(a, plan, B, st);
+    return plan.smem_tables ? launch_refine_t<true, uint32_t, false, CT>(a, plan, B, st)
+                            : launch_refine_t<false, uint32_t, false, CT>(a, plan, B, st);
 }
 
 int launch_refine(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st) {
     if (B == 0) return 0;
-    if (plan.m8) return plan.smem_tables ? launch_refine_t<true, uint16_t, true>(a, plan, B, st)
-                                         : launch_refine_t<false, uint16_t, true>(a, plan, B, st);
-    if (key16) return plan.smem_tables ? launch_refine_t<true, uint16_t, false>(a, plan, B, st)
-                                       : launch_refine_t<false, uint16_t, false>(a, plan, B, st);
-    return plan.smem_tables ? launch_refine_t<true, uint32_t, false>(a, plan, B, st)
-                            : launch_refine_t<false, uint32_t, false>(a, plan, B, st);
+    return plan.cta ? launch_refine_c<true>(a, plan, B, key16, st) : launch_refine_c<false>(a, plan, B, key16, st);
 }
 
 int launch_crossover(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs, int16_t* out, int B,

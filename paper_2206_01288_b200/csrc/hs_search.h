@@ -24,6 +24,9 @@ struct GAArgs {
     const double* vals;
     HKTables hk;
     int pop, generations, kind /*0 ours 1 kl 2 none*/, max_passes, patience /*<=0: none*/;
+    HKBig hkb;            // d_pp > 8: CTA pricing schedule
+    double* hk_scratch;   // d_pp > 8: per-island Held-Karp slices
+    size_t hk_size;
     int gen_end;   // run generations [state.gen, gen_end)
     int finalize;  // price the canonical best when the run is over
     GAState* state;      // [islands]
@@ -45,6 +48,9 @@ struct RefineArgs {
     const void* rank;
     const double* vals;
     HKTables hk;
+    HKBig hkb;
+    double* hk_scratch;
+    size_t hk_size;
     int kind, max_passes, single_pass, phase;
     const int16_t* groups;  // [B][k*m]
     hs_pcg64* rng;          // [B] in/out
@@ -62,7 +68,7 @@ struct SearchShape {
 
 struct SearchPlan {
     int warps;
-    bool smem_tables, m8;
+    bool smem_tables, m8, cta;
     size_t smem;
 };
 

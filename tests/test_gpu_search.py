@@ -212,3 +212,32 @@ def test_evolve_errors_like_reference():
         S.evolve(g, w, S.ScheduleConfig(pop_size=4, generations=3, local_search="ours"))
     res = S.evolve(g, w, S.ScheduleConfig(pop_size=4, generations=3, local_search="kl"))
     assert res.best_cost.pipelinep == 0.0
+
+
+@pytest.mark.parametrize("name,kind,pop,gens", [("r32_16x2", "ours", 8, 12), ("r32_16x2", "kl", 8, 12),
+                                                ("r48_12x4", "ours", 8, 6), ("r18_9x2", "ours", 8, 15),
+                                                ("config4", "kl", 4, 2)])
+def test_evolve_d_pp_above_8_vs_oracle(name, kind, pop, gens):
+    """GA with CTA-level pricing (d_pp 9..16) reproduces the oracle's evolve."""
+    g, w = I.instance(name)
+    cfg = S.ScheduleConfig(pop_size=pop, generations=gens, local_search=kind, seed=4)
+    r = S.evolve(g, w, cfg)
+    o = O.Oracle.of(g, w).evolve(pop, gens, kind, seed=4)
+    assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+    assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+    assert list(r.best_cost.pipeline_order.order) == list(o["order"])
+    assert [t[1] for t in r.trace] == list(o["trace_best"])
+    assert [t[2] for t in r.trace] == list(o["trace_mean"])
+
+
+def test_local_search_d_pp_16_vs_oracle():
+    g, w = I.instance("r32_16x2")
+    rng = np.random.default_rng(1)
+    for t in range(3):
+        p = S.random_partition(rng, g.n, w.d_pp, w.d_dp)
+        for kind in ("ours", "kl"):
+            r1 = np.random.default_rng(50 + t)
+            st = O.rng_state(np.random.default_rng(50 + t))
+            out = S.local_search(g, w, p, kind=kind, rng=r1)
+            want = O.Oracle.of(g, w).local_search(np.array(p.groups, dtype=np.int32), kind, st)
+            assert [list(x) for x in out.groups] == want.tolist()
