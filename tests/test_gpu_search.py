@@ -26,7 +26,7 @@ def _rng_tuple(rng):
 
 def _gpu_ok(name):
     k, m = I.meta()[name]["recipe"]["w"][:2]
-    return k <= 8 and m <= 64
+    return k <= 16 and m <= 64
 
 
 def test_surrogate_weights_and_g4_gains():
