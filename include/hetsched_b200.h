@@ -130,6 +130,22 @@ int hs_gains(int n, int d_pp, int d_dp, int device, const double *sw, int kind, 
  * members ascending) */
 int hs_random_partitions(int n, int d_pp, int d_dp, int device, int B, hs_pcg64 *rng, int16_t *out);
 
+/* ---------------- fixed layouts (evaluation.py) ---------------------------- */
+
+/* materialize (evaluation.py:162-192): grid int16 [B][d_dp][d_pp] (row i =
+ * macro-batch chain, column b = stage) and stage order int8 [B][d_pp] of B
+ * partitions, using the lexicographically smallest bottleneck pairing
+ * (combinatorics.py:147-189) between consecutive stages; host buffers,
+ * d_pp <= 8. */
+int hs_materialize(hs_instance *h, int64_t B, const int16_t *groups, int16_t *grid, int8_t *order);
+/* evaluate_assignment (evaluation.py:195-229) of B grids int16
+ * [B][d_dp][d_pp]: out3 [B][3] (total, datap, pipelinep), per_col [B][d_pp]
+ * (nullable); host buffers.  Grids must be valid assignments. */
+int hs_evaluate_assignments(hs_instance *h, int64_t B, const int16_t *grids, double *out3, double *per_col);
+/* random_assignment (evaluation.py:232-243) for B independent streams:
+ * grids int16 [B][d_dp][d_pp], orders int8 [B][d_pp]; host buffers. */
+int hs_random_assignments(int n, int d_pp, int d_dp, int device, int B, hs_pcg64 *rng, int16_t *grids, int8_t *orders);
+
 #ifdef __cplusplus
 }
 #endif

@@ -112,6 +112,9 @@ def lib():
         L.hs_crossover.argtypes = [i32, i32, i32, i32, i32, vp, vp, pcg, vp]
         L.hs_gains.argtypes = [i32, i32, i32, i32, vp, i32, i32, vp, vp, vp]
         L.hs_random_partitions.argtypes = [i32, i32, i32, i32, i32, pcg, vp]
+        L.hs_materialize.argtypes = [vp, i64, vp, vp, vp]
+        L.hs_evaluate_assignments.argtypes = [vp, i64, vp, vp, vp]
+        L.hs_random_assignments.argtypes = [i32, i32, i32, i32, i32, pcg, vp, vp]
         for name in EXPORTS:
             if name not in ("hs_version", "hs_last_error"):
                 getattr(L, name).restype = i32
@@ -122,7 +125,8 @@ def lib():
 EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_destroy", "hs_instance_tables",
            "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_run",
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
-           "hs_crossover", "hs_gains", "hs_random_partitions")
+           "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
+           "hs_random_assignments")
 
 
 def check(rc: int, what: str) -> None:
