@@ -1,5 +1,7 @@
 // hs_capi_search.cu -- C-ABI of the search kernels (include/hetsched_b200.h).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "hs_big.h"
@@ -62,6 +64,7 @@ struct hs_ga {
     int8_t* out_order = nullptr;
     int16_t* out_groups = nullptr;
     double* hk_scratch = nullptr;
+    long long* prof = nullptr;  // HS_GA_PROFILE=1: driver-phase cycle counters of island 0
 };
 
 static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
@@ -95,6 +98,7 @@ static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
     a.hkb = h->hkb;
     a.hk_scratch = ga->hk_scratch;
     a.hk_size = h->k > 8 ? hs::hk_big_size(h->k) : 0;
+    a.prof = ga->prof;
     return a;
 }
 
@@ -135,6 +139,10 @@ int hs_ga_create(hs_instance* h, const hs_ga_config* cfg, int islands, const hs_
     CK(cudaMalloc(&ga->out_groups, (size_t)islands * km * 2), "cudaMalloc");
     if (h->k > 8) CK(cudaMalloc(&ga->hk_scratch, (size_t)islands * hs::hk_big_size(h->k) * 8), "cudaMalloc");
     CK(cudaMemcpy(ga->state, st.data(), sizeof(hs::GAState) * islands, cudaMemcpyHostToDevice), "upload state");
+    if (getenv("HS_GA_PROFILE")) {
+        CK(cudaMalloc(&ga->prof, 16 * sizeof(long long)), "cudaMalloc");
+        CK(cudaMemset(ga->prof, 0, 16 * sizeof(long long)), "memset");
+    }
     *out = ga;
     return 0;
 }
@@ -191,6 +199,15 @@ int hs_ga_result(hs_ga* ga, int16_t* best_groups, double* best3, double* best_pe
     if (best_order) CK(cudaMemcpy(best_order, ga->out_order, (size_t)I * k, cudaMemcpyDeviceToHost), "D2H");
     if (trace_best) CK(cudaMemcpy(trace_best, ga->trace_best, (size_t)I * G * 8, cudaMemcpyDeviceToHost), "D2H");
     if (trace_mean) CK(cudaMemcpy(trace_mean, ga->trace_mean, (size_t)I * G * 8, cudaMemcpyDeviceToHost), "D2H");
+    if (ga->prof) {
+        long long pv[16];
+        CK(cudaMemcpy(pv, ga->prof, sizeof(pv), cudaMemcpyDeviceToHost), "D2H");
+        fprintf(stderr,
+                "[hs_ga_profile] cycles: crossover %lld sweep %lld chains %lld price %lld | chain rounds %lld "
+                "(caches at start %lld) moves %lld (cache refresh %lld) | best_candidate %lld calls %lld cycles, "
+                "swaps %lld, fast_edge computes %lld (%lld cycles)\n",
+                pv[0], pv[1], pv[2], pv[3], pv[5], pv[4], pv[7], pv[6], pv[8], pv[12], pv[11], pv[10], pv[9]);
+    }
     for (int i = 0; i < I; i++) {
         if (trace_len) trace_len[i] = st[i].gen;
         if (evaluations) evaluations[i] = st[i].evaluations;
@@ -204,7 +221,7 @@ int hs_ga_destroy(hs_ga* ga) {
     DeviceGuard dg(ga->h->device);
     for (void* p : {(void*)ga->state, (void*)ga->pop, (void*)ga->cost, (void*)ga->best, (void*)ga->trace_best,
                     (void*)ga->trace_mean, (void*)ga->out3, (void*)ga->out_pg, (void*)ga->out_order,
-                    (void*)ga->out_groups, (void*)ga->hk_scratch})
+                    (void*)ga->out_groups, (void*)ga->hk_scratch, (void*)ga->prof})
         if (p) cudaFree(p);
     delete ga;
     return 0;

@@ -64,9 +64,12 @@ struct LS {
     const double* W;  // surrogate weights n x n (scheduler.py:84-88)
     int16_t* G;       // k x cap members, ascending
     int* sz;          // k sizes
-    double* mean;     // n x k: mean[u*k+i] = seq_sum(W[u, G_i]) / sz_i
+    double* mean;     // n x k: mean[u*k+i] = seq_sum(W[u, G_i]) / sz_i, computed lazily
+    uint32_t* mver;   // n x k: version of the group a mean entry was computed for
+    uint32_t* cver;   // k: group content versions (bumped on every change)
     double* home;     // n: cheapest intra-group link of each device
-    int* valid;       // [0]: mean columns valid (bitmask), [1]: home groups valid
+    int* valid;       // [0]: mean columns valid, [1]: home groups valid, [2]: fast edges valid (bitmasks)
+    int16_t* fe;      // k x 2 cached _fast_edge pairs
     uint32_t* locked;  // n-bit set
     int* nlocked;
     int16_t* perm;    // C(k,2)
@@ -94,6 +97,82 @@ __device__ __forceinline__ void g_insort(LS& s, int j, int d) {  // bisect.insor
     s.sz[j]++;
 }
 
+// _move (:294-296) by the whole warp: remove v from src, insort into dst.
+// Members are distinct and ascending, so each element's new slot is its old
+// index shifted by one past the removal / insertion point (ballots).
+__device__ __forceinline__ void g_move_w(LS& s, int v, int src, int dst, int lane) {
+    int16_t* gs = s.G + src * s.cap;
+    int16_t* gd = s.G + dst * s.cap;
+    const int cs = s.sz[src], cd = s.sz[dst];
+    int16_t a[3], b[3];
+    int below = 0, pos = INT_MAX;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        int i = lane + 32 * q;
+        a[q] = i < cs ? gs[i] : (int16_t)0x7fff;
+        b[q] = i < cd ? gd[i] : (int16_t)0x7fff;
+        unsigned hit = __ballot_sync(kFull, i < cs && a[q] == v);
+        if (hit && pos == INT_MAX) pos = 32 * q + __ffs(hit) - 1;
+        below += __popc(__ballot_sync(kFull, i < cd && b[q] < v));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        int i = lane + 32 * q;
+        if (i < cs && i != pos) gs[i < pos ? i : i - 1] = a[q];
+        if (i < cd) gd[i < below ? i : i + 1] = b[q];
+    }
+    if (lane == 0) {
+        gd[below] = (int16_t)v;
+        s.sz[src] = cs - 1;
+        s.sz[dst] = cd + 1;
+    }
+    __syncwarp();
+}
+
+// x / cnt, IEEE-exact: for a power-of-two count the reciprocal is exact, so
+// the product is the same correctly rounded quotient.
+__device__ __forceinline__ double div_count(double x, int cnt) {
+    return (cnt & (cnt - 1)) == 0 ? x * (1.0 / (double)cnt) : x / (double)cnt;
+}
+
+// _swap (:252-257) by the whole warp, both groups in one pass: group j loses
+// a and gains b, group j2 loses b and gains a.  New slot of a surviving
+// member x: idx - (out < x) + (in < x); the incomer lands after every
+// survivor below it.
+__device__ __forceinline__ void swap_one(int16_t* g, int c, int out, int in, int lane) {
+    int16_t x[3];
+    int below = 0;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        int i = lane + 32 * q;
+        x[q] = i < c ? g[i] : (int16_t)0x7fff;
+        if (32 * q < c) below += __popc(__ballot_sync(kFull, i < c && x[q] != out && x[q] < in));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        int i = lane + 32 * q;
+        if (i < c && x[q] != out) g[i - (out < x[q]) + (in < x[q])] = x[q];
+    }
+    if (lane == 0) g[below] = (int16_t)in;
+    __syncwarp();
+}
+
+__device__ __forceinline__ void g_swap_w(LS& s, int a, int j, int b, int j2, int lane) {
+    swap_one(s.G + j * s.cap, s.sz[j], a, b, lane);
+    swap_one(s.G + j2 * s.cap, s.sz[j2], b, a, lane);
+}
+
+// numpy pairwise sum of exactly 8 lane-held values (lanes 8q..8q+7): the
+// xor-1/2/4 butterfly is the ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree.
+__device__ __forceinline__ double butterfly8(double x) {
+    x += __shfl_xor_sync(kFull, x, 1);
+    x += __shfl_xor_sync(kFull, x, 2);
+    x += __shfl_xor_sync(kFull, x, 4);
+    return x;
+}
+
 __device__ __forceinline__ double row_pw(const LS& s, int u, const int16_t* grp, int cnt) {
     const double* wr = s.W + (size_t)u * s.n;
     if (cnt < 8) {
@@ -106,22 +185,62 @@ __device__ __forceinline__ double row_pw(const LS& s, int u, const int16_t* grp,
 
 __device__ __forceinline__ double row_seq_mean(const LS& s, int u, const int16_t* grp, int cnt) {
     const double* wr = s.W + (size_t)u * s.n;
-    double r = 0.0;
-    for (int i = 0; i < cnt; i++) r += wr[grp[i]];
-    return r / (double)cnt;
+    double r = 0.0;  // sequential: w[:, grp].mean(axis=1) reduces an F-contiguous array
+    int i = 0;
+    for (; i + 4 <= cnt; i += 4) {
+        double w0 = wr[grp[i]], w1 = wr[grp[i + 1]], w2 = wr[grp[i + 2]], w3 = wr[grp[i + 3]];
+        r += w0;
+        r += w1;
+        r += w2;
+        r += w3;
+    }
+    for (; i < cnt; i++) r += wr[grp[i]];
+    return div_count(r, cnt);
 }
 
-// _fast_edge (:237-249): lexicographically first minimum intra-group pair
-__device__ inline void fast_edge(const LS& s, int j, int lane, int& a, int& b) {
+// mean[u][i] (_group_means, scheduler.py:279-284) on demand
+__device__ __forceinline__ double mean_at(LS& s, int u, int i) {
+    const int x = u * s.k + i;
+    const uint32_t ver = s.cver[i];
+    if (s.mver[x] != ver) {
+        s.mean[x] = row_seq_mean(s, u, s.G + i * s.cap, s.sz[i]);
+        s.mver[x] = ver;
+    }
+    return s.mean[x];
+}
+
+__device__ long long* g_prof = nullptr;
+
+// _fast_edge (:237-249): lexicographically first minimum intra-group pair,
+// lanes over (i, l) pairs, cached per group until the group changes.
+__device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
+    if (s.valid[2] >> j & 1) {
+        a = s.fe[2 * j];
+        b = s.fe[2 * j + 1];
+        return;
+    }
+    long long f0 = clock64();
     const int16_t* g = s.G + j * s.cap;
-    int c = s.sz[j];
+    const int c = s.sz[j];
     double bv = kInf;
     int code = INT_MAX;
-    for (int i = lane; i < c; i += kWarp) {
-        const double* wr = s.W + (size_t)g[i] * s.n;
-        for (int l = i + 1; l < c; l++) {
-            double v = wr[g[l]];
-            if (v < bv) {
+    if (c == 8) {
+        if (lane < 28) {  // lane -> (i, l), i < l, lexicographic
+            int i = 0, t = lane;
+            while (t >= 7 - i) {
+                t -= 7 - i;
+                i++;
+            }
+            int l = i + 1 + t;
+            bv = s.W[(size_t)g[i] * s.n + g[l]];
+            code = i * 256 + l;
+        }
+    } else {
+        for (int t = lane; t < c * c; t += kWarp) {
+            int i = t / c, l = t - (t / c) * c;
+            if (l <= i) continue;
+            double v = s.W[(size_t)g[i] * s.n + g[l]];
+            if (v < bv) {  // t ascends per lane, so strict < keeps the first
                 bv = v;
                 code = i * 256 + l;
             }
@@ -131,29 +250,55 @@ __device__ inline void fast_edge(const LS& s, int j, int lane, int& a, int& b) {
     if (code == INT_MAX) code = 1;  // (grp[0], grp[1]) default
     a = g[code >> 8];
     b = g[code & 255];
+    __syncwarp();
+    if (lane == 0) {
+        s.fe[2 * j] = (int16_t)a;
+        s.fe[2 * j + 1] = (int16_t)b;
+        s.valid[2] |= 1 << j;
+        if (g_prof) {
+            g_prof[9] += clock64() - f0;
+            g_prof[10] += 1;
+        }
+    }
+    __syncwarp();
 }
 
 // _best_candidate (:260-276) with _gain_ours (:206-209): the four candidates
 // need only four row sums, computed by lanes 0..3.
-__device__ inline double best_candidate(const LS& s, int j, int j2, int lane, int& oa, int& ob) {
+__device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa, int& ob) {
     int d1, d2, d1p, d2p;
     fast_edge(s, j, lane, d1, d2);
     fast_edge(s, j2, lane, d1p, d2p);
     const int16_t* gj = s.G + j * s.cap;
     const int16_t* gj2 = s.G + j2 * s.cap;
     int cj = s.sz[j], cj2 = s.sz[j2];
-    double sum = 0.0;
-    if (lane < 4) {
-        int u = lane == 0 ? d1 : lane == 1 ? d2 : lane == 2 ? d1p : d2p;
-        sum = lane < 2 ? row_pw(s, u, gj2, cj2) : row_pw(s, u, gj, cj);
+    double S0, S1, S2, S3;
+    if (cj == 8 && cj2 == 8) {
+        // four 8-term pairwise sums at once: lanes 8q..8q+7 hold one row each
+        const int q = lane >> 3, e = lane & 7;
+        const int u = q == 0 ? d1 : q == 1 ? d2 : q == 2 ? d1p : d2p;
+        const int16_t* gg = q < 2 ? gj2 : gj;
+        double x = butterfly8(s.W[(size_t)u * s.n + gg[e]]);
+        S0 = __shfl_sync(kFull, x, 0);
+        S1 = __shfl_sync(kFull, x, 8);
+        S2 = __shfl_sync(kFull, x, 16);
+        S3 = __shfl_sync(kFull, x, 24);
+    } else {
+        double sum = 0.0;
+        if (lane < 4) {
+            int u = lane == 0 ? d1 : lane == 1 ? d2 : lane == 2 ? d1p : d2p;
+            sum = lane < 2 ? row_pw(s, u, gj2, cj2) : row_pw(s, u, gj, cj);
+        }
+        S0 = __shfl_sync(kFull, sum, 0);
+        S1 = __shfl_sync(kFull, sum, 1);
+        S2 = __shfl_sync(kFull, sum, 2);
+        S3 = __shfl_sync(kFull, sum, 3);
     }
-    double S0 = __shfl_sync(kFull, sum, 0), S1 = __shfl_sync(kFull, sum, 1);
-    double S2 = __shfl_sync(kFull, sum, 2), S3 = __shfl_sync(kFull, sum, 3);
     const int n = s.n;
-    double t1a = S0 / (double)cj2 - s.W[(size_t)d1 * n + d2];   // a = d1, pa = d2
-    double t1b = S1 / (double)cj2 - s.W[(size_t)d2 * n + d1];   // a = d2, pa = d1
-    double t2a = S2 / (double)cj - s.W[(size_t)d1p * n + d2p];  // b = d1p, pb = d2p
-    double t2b = S3 / (double)cj - s.W[(size_t)d2p * n + d1p];  // b = d2p, pb = d1p
+    double t1a = div_count(S0, cj2) - s.W[(size_t)d1 * n + d2];   // a = d1, pa = d2
+    double t1b = div_count(S1, cj2) - s.W[(size_t)d2 * n + d1];   // a = d2, pa = d1
+    double t2a = div_count(S2, cj) - s.W[(size_t)d1p * n + d2p];  // b = d1p, pb = d2p
+    double t2b = div_count(S3, cj) - s.W[(size_t)d2p * n + d1p];  // b = d2p, pb = d1p
     double g[4] = {t1a + t2a, t1a + t2b, t1b + t2a, t1b + t2b};
     int A[4] = {d1, d1, d2, d2}, Bv[4] = {d1p, d2p, d1p, d2p};
     double best = -kInf;
@@ -170,8 +315,9 @@ __device__ inline double best_candidate(const LS& s, int j, int j2, int lane, in
 }
 
 __device__ __forceinline__ void invalidate(LS& s, int j) {
-    s.valid[0] &= ~(1 << j);
     s.valid[1] &= ~(1 << j);
+    s.valid[2] &= ~(1 << j);
+    s.cver[j]++;
 }
 
 // even phase of _pass_ours: swap sweep over rng.permutation(C(k,2)) pairs
@@ -193,13 +339,16 @@ __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
         decode_pair(s.perm[q], k, j, j2);
         for (int it = 0; it < d_dp; it++) {
             int a, b;
+            long long b0 = clock64();
             double gain = best_candidate(s, j, j2, lane, a, b);
+            if (g_prof && lane == 0) {
+                g_prof[8] += 1;
+                g_prof[12] += clock64() - b0;
+                g_prof[11] += gain > 0.0;
+            }
             if (gain <= 0.0) break;
-            if (lane == 0) {  // _swap (:252-257)
-                g_remove(s, j, a);
-                g_remove(s, j2, b);
-                g_insort(s, j2, a);
-                g_insort(s, j, b);
+            g_swap_w(s, a, j, b, j2, lane);  // _swap (:252-257)
+            if (lane == 0) {
                 invalidate(s, j);
                 invalidate(s, j2);
             }
@@ -210,28 +359,25 @@ __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
     return changed;
 }
 
+// _home_costs (:287-291) for every group whose members changed
 __device__ inline void ensure_caches(LS& s, int lane) {
     const int k = s.k, n = s.n;
-    int mv = s.valid[0], hv = s.valid[1];
+    const int hv = s.valid[1];
+    if (hv == (1 << k) - 1) return;
     for (int i = 0; i < k; i++) {
+        if (hv >> i & 1) continue;
         const int16_t* g = s.G + i * s.cap;
-        int c = s.sz[i];
-        if (!(mv >> i & 1))
-            for (int u = lane; u < n; u += kWarp) s.mean[u * k + i] = row_seq_mean(s, u, g, c);
-        if (!(hv >> i & 1))
-            for (int a = lane; a < c; a += kWarp) {  // _home_costs (:287-291)
-                const double* wr = s.W + (size_t)g[a] * n;
-                double h = kInf;
-                for (int b = 0; b < c; b++)
-                    if (b != a) h = dmin(h, wr[g[b]]);
-                s.home[g[a]] = h;
-            }
+        const int c = s.sz[i];
+        for (int a = lane; a < c; a += kWarp) {
+            const double* wr = s.W + (size_t)g[a] * n;
+            double h = kInf;
+            for (int b = 0; b < c; b++)
+                if (b != a) h = dmin(h, wr[g[b]]);
+            s.home[g[a]] = h;
+        }
     }
     __syncwarp();
-    if (lane == 0) {
-        s.valid[0] = (1 << k) - 1;
-        s.valid[1] = (1 << k) - 1;
-    }
+    if (lane == 0) s.valid[1] = (1 << k) - 1;
     __syncwarp();
 }
 
@@ -255,10 +401,37 @@ __device__ __forceinline__ int fastest_free(const LS& s, int i, double& home) {
     return best;
 }
 
-// _chain_round (:299-391)
+// fastest_free over the warp: lanes over members, min by (home, id)
+__device__ __forceinline__ int fastest_free_w(const LS& s, int i, int lane, double& home) {
+    const int16_t* g = s.G + i * s.cap;
+    const int c = s.sz[i];
+    if (c < 2) return -1;
+    double bh = kInf;
+    int bd = INT_MAX;
+    for (int a = lane; a < c; a += kWarp) {
+        int d = g[a];
+        if (s.locked[d >> 5] >> (d & 31) & 1) continue;
+        double h = s.home[d];
+        if (h < bh || (h == bh && d < bd)) {
+            bh = h;
+            bd = d;
+        }
+    }
+    warp_argmin(bh, bd);
+    home = bh;
+    return bd == INT_MAX ? -1 : bd;
+}
+
+// _chain_round (:299-391).  All lanes run the control flow uniformly; the
+// member scans, target argmax and group moves are lane-parallel.
 __device__ __noinline__ bool chain_round(LS& s, int lane) {
-    const int k = s.k, n = s.n;
+    const int k = s.k;
+    long long c0 = clock64();
     ensure_caches(s, lane);
+    if (g_prof && lane == 0) {
+        g_prof[4] += clock64() - c0;
+        g_prof[5] += 1;
+    }
     // start group: largest relocation gain, first on ties
     double gain = -kInf;
     int idx = INT_MAX;
@@ -270,7 +443,7 @@ __device__ __noinline__ bool chain_round(LS& s, int lane) {
             bool first = true;
             for (int j = 0; j < k; j++) {
                 if (j == lane) continue;
-                double x = s.mean[v * k + j];
+                double x = mean_at(s, v, j);
                 if (first || x > mx) mx = x;
                 first = false;
             }
@@ -284,103 +457,77 @@ __device__ __noinline__ bool chain_round(LS& s, int lane) {
     int* mv_v = s.i32;
     int* mv_src = s.i32 + k;
     int* mv_dst = s.i32 + 2 * k;
-    int* ctl = s.i32 + 3 * k;  // [0]=nm [1]=natural [2]=cur [3]=done
     double* steps = s.f64;
     double* closers = s.f64 + k + 1;
-    if (lane == 0) {
-        ctl[0] = 0;
-        ctl[1] = 0;
-        ctl[2] = start;
-        ctl[3] = 0;
-    }
-    __syncwarp();
+    int cur = start, nm = 0;
+    bool natural = false;
     for (int it = 0; it < k; it++) {
-        if (lane == 0) {
-            int cur = ctl[2];
-            double home;
-            int v = fastest_free(s, cur, home);
-            if (v < 0) {
-                ctl[3] = 1;
-            } else {
-                int dst = -1;
-                double sc = -kInf;
-                for (int j = 0; j < k; j++) {
-                    if (j == cur) continue;
-                    double x = s.mean[v * k + j];
-                    if (dst < 0 || x > sc) {
-                        sc = x;
-                        dst = j;
-                    }
-                }
-                int nm = ctl[0];
-                closers[nm] = cur != start ? s.mean[v * k + start] - home : -kInf;
-                steps[nm] = sc - home;
-                g_remove(s, cur, v);  // _move (:294-296)
-                g_insort(s, dst, v);
-                s.locked[v >> 5] |= 1u << (v & 31);
-                s.nlocked[0]++;
-                mv_v[nm] = v;
-                mv_src[nm] = cur;
-                mv_dst[nm] = dst;
-                ctl[0] = nm + 1;
-                ctl[2] = dst;
-                s.valid[0] &= ~((1 << cur) | (1 << dst));
-                s.valid[1] &= ~((1 << cur) | (1 << dst));
-                if (dst == start) {
-                    ctl[1] = 1;
-                    ctl[3] = 1;
-                }
-            }
+        double home;
+        const int v = fastest_free_w(s, cur, lane, home);
+        if (v < 0) break;
+        double sc = -kInf;
+        int dst = INT_MAX;
+        if (lane < k && lane != cur) {
+            sc = mean_at(s, v, lane);
+            dst = lane;
         }
+        warp_argmax(sc, dst);  // first maximum over targets
         __syncwarp();
+        if (lane == 0) {
+            closers[nm] = cur != start ? mean_at(s, v, start) - home : -kInf;
+            steps[nm] = sc - home;
+            mv_v[nm] = v;
+            mv_src[nm] = cur;
+            mv_dst[nm] = dst;
+            s.locked[v >> 5] |= 1u << (v & 31);
+            s.nlocked[0]++;
+            invalidate(s, cur);
+            invalidate(s, dst);
+        }
+        g_move_w(s, v, cur, dst, lane);
+        nm++;
         // refresh the touched mean columns and home costs (scheduler.py:362-363)
+        long long c1 = clock64();
         ensure_caches(s, lane);
-        if (ctl[3]) break;
+        if (g_prof && lane == 0) {
+            g_prof[6] += clock64() - c1;
+            g_prof[7] += 1;
+        }
+        cur = dst;
+        if (cur == start) {
+            natural = true;
+            break;
+        }
     }
-    const int nm = ctl[0];
     if (nm == 0) return false;
-    bool applied = false;
+    double prefix = 0.0, best_v = -kInf;
+    int best_l = -1;
+    // prefix[l] = cumsum of steps[0..l-1] (np.cumsum, sequential)
+    for (int l = 0; l < nm; l++) {
+        double value = prefix + closers[l];
+        if (value > best_v) {
+            best_v = value;
+            best_l = l;
+        }
+        prefix = prefix + steps[l];
+    }
+    if (natural && prefix > best_v) {
+        best_v = prefix;
+        best_l = nm;
+    }
+    const bool applied = best_v > 0.0;
+    const int keep = applied ? best_l : 0;
+    for (int t = nm - 1; t >= keep; t--) g_move_w(s, mv_v[t], mv_dst[t], mv_src[t], lane);
+    if (applied && best_l < nm) g_move_w(s, mv_v[best_l], mv_src[best_l], start, lane);
     if (lane == 0) {
-        double prefix = 0.0, best_v = -kInf;
-        int best_l = -1;
-        // prefix[l] = cumsum of steps[0..l-1] (np.cumsum, sequential)
-        for (int l = 0; l < nm; l++) {
-            double value = prefix + closers[l];
-            if (value > best_v) {
-                best_v = value;
-                best_l = l;
-            }
-            prefix = prefix + steps[l];
-        }
-        if (ctl[1] && prefix > best_v) {
-            best_v = prefix;
-            best_l = nm;
-        }
-        if (best_v <= 0.0) {
-            for (int t = nm - 1; t >= 0; t--) {
-                g_remove(s, mv_dst[t], mv_v[t]);
-                g_insort(s, mv_src[t], mv_v[t]);
-            }
-        } else {
-            for (int t = nm - 1; t >= best_l; t--) {
-                g_remove(s, mv_dst[t], mv_v[t]);
-                g_insort(s, mv_src[t], mv_v[t]);
-            }
-            if (best_l < nm) {
-                g_remove(s, mv_src[best_l], mv_v[best_l]);
-                g_insort(s, start, mv_v[best_l]);
-            }
-            applied = true;
-        }
         for (int t = 0; t < nm; t++) {
             invalidate(s, mv_src[t]);
             invalidate(s, mv_dst[t]);
         }
         invalidate(s, start);
-        ctl[4] = applied;
     }
     __syncwarp();
-    return ctl[4] != 0;
+    return applied;
 }
 
 // odd phase of _pass_ours: chains until every device is locked
@@ -435,12 +582,10 @@ __device__ __noinline__ bool pass_kl(LS& s, int lane) {
             }
             warp_argmax(bg, bt);
             if (bg > 0.0) {
+                const int a = a1[bt / c2], b = a2[bt % c2];
+                __syncwarp();
+                g_swap_w(s, a, j, b, j2, lane);  // _swap (:252-257)
                 if (lane == 0) {
-                    int a = a1[bt / c2], b = a2[bt % c2];
-                    g_remove(s, j, a);
-                    g_remove(s, j2, b);
-                    g_insort(s, j2, a);
-                    g_insort(s, j, b);
                     invalidate(s, j);
                     invalidate(s, j2);
                 }
@@ -455,9 +600,11 @@ __device__ __noinline__ bool pass_kl(LS& s, int lane) {
 __device__ __forceinline__ void load_groups(LS& s, const int16_t* p, int lane) {
     for (int t = lane; t < s.k * s.m; t += kWarp) s.G[(t / s.m) * s.cap + t % s.m] = p[t];
     if (lane < s.k) s.sz[lane] = s.m;
+    if (lane < s.k) s.cver[lane]++;
     if (lane == 0) {
         s.valid[0] = 0;
         s.valid[1] = 0;
+        s.valid[2] = 0;
     }
     __syncwarp();
 }
@@ -681,8 +828,13 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
+    s.mver = reinterpret_cast<uint32_t*>(take((size_t)n * k * 4));
+    s.cver = reinterpret_cast<uint32_t*>(take((size_t)k * 4));
+    for (int t = threadIdx.x; t < n * k; t += blockDim.x) s.mver[t] = 0;
+    for (int t = threadIdx.x; t < k; t += blockDim.x) s.cver[t] = 1;
     s.home = reinterpret_cast<double*>(take((size_t)n * 8));
-    s.valid = reinterpret_cast<int*>(take(8));
+    s.valid = reinterpret_cast<int*>(take(16));
+    s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
     s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
     s.nlocked = reinterpret_cast<int*>(take(4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
@@ -700,6 +852,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     Pcg64 rng;
     if (wid == 0) rng.load(st.rng);
     const bool driver = wid == 0;
+    if (a.prof && isl == 0 && threadIdx.x == 0) g_prof = a.prof;
 
     if (!st.initialized) {
         // init_population (scheduler.py:124-136): sequential random_partition
@@ -786,17 +939,23 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             copy16(g.par, pop + (size_t)i * km, km, lane);
             copy16(g.par + km, pop + (size_t)i2 * km, km, lane);
             __syncwarp();
+            long long t0 = clock64();
             crossover(s, g.par, g.par + km, rng, g.snaps, lane);
+            long long t1 = clock64();
+            if (a.prof && isl == 0 && lane == 0) a.prof[0] += t1 - t0;
             int nsnap = 1;
             if (a.kind != 2) {  // _refine (:455-487)
                 load_groups(s, g.snaps, lane);
                 int stale = 0;
                 for (int t = 0; t < a.max_passes; t++) {
                     bool changed;
+                    long long p0 = clock64();
                     if (a.kind == 0)
                         changed = (s.sz[0] < 2) ? false : (t % 2 == 0 ? pass_sweep(s, rng, lane) : pass_chains(s, lane));
                     else
                         changed = pass_kl(s, lane);
+                    long long p1 = clock64();
+                    if (a.prof && isl == 0 && lane == 0) a.prof[1 + (t & 1)] += p1 - p0;
                     if (!changed) {
                         stale++;
                         if (stale >= stop_after) break;
@@ -809,10 +968,12 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             }
             if (lane == 0) g.ctl[0] = nsnap;
         }
+        long long q0 = clock64();
         __syncthreads();
         const int nsnap = g.ctl[0];
         pr.all(g.snaps, nsnap, km, g.snapcost, wid, W, lane);
         __syncthreads();
+        if (a.prof && isl == 0 && threadIdx.x == 0) a.prof[3] += clock64() - q0;
         if (driver) {
             int bsi = 0, worst = 0, replace = 0, improve = 0;
             double cb = 0.0;
@@ -933,8 +1094,13 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
+    s.mver = reinterpret_cast<uint32_t*>(take((size_t)n * k * 4));
+    s.cver = reinterpret_cast<uint32_t*>(take((size_t)k * 4));
+    for (int t = threadIdx.x; t < n * k; t += blockDim.x) s.mver[t] = 0;
+    for (int t = threadIdx.x; t < k; t += blockDim.x) s.cver[t] = 1;
     s.home = reinterpret_cast<double*>(take((size_t)n * 8));
-    s.valid = reinterpret_cast<int*>(take(8));
+    s.valid = reinterpret_cast<int*>(take(16));
+    s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
     s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
     s.nlocked = reinterpret_cast<int*>(take(4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
@@ -1072,7 +1238,9 @@ __global__ void gains_kernel(int n, int k, int m, const double* __restrict__ sw,
 static size_t ls_bytes(int n, int k, int m) {
     int cap = m + 1;
     auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
-    return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)n * k * 8) + al((size_t)n * 8) + al(8) +
+    return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)n * k * 8) + al((size_t)n * k * 4) +
+           al((size_t)k * 4) + al((size_t)n * 8) + al(16) +
+           al((size_t)k * 4) +
            al((size_t)((n + 31) >> 5) * 4) + al(4) + al((size_t)(k * k + cap) * 2) +
            al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
 }

@@ -39,6 +39,7 @@ struct GAArgs {
     double* out_pg;      // [islands][k]
     int8_t* out_order;   // [islands][k]
     int16_t* out_groups; // [islands][k*m] canonical best
+    long long* prof;     // optional driver-phase cycle counters (island 0), see hs_search.cu
 };
 
 struct RefineArgs {
