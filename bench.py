@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ga", action="store_true", help="skip the GA time-to-converge / island legs")
-    ap.add_argument("--islands", type=int, default=0, help="GA islands per GPU (default: one per SM)")
+    ap.add_argument("--islands", type=int, default=0, help="GA islands per GPU (default: 8 per SM, one per warp)")
     ap.add_argument("--island-gens", type=int, default=100)
     return ap.parse_args()
 
@@ -326,7 +326,7 @@ def ga_legs(g, w, rank, world, local, barrier, dist):
         "reference_python_seconds_build_container": ref_s,
     }
     sms = torch.cuda.get_device_properties(local).multi_processor_count
-    I = ARGS.islands or sms
+    I = ARGS.islands or sms * 8
     icfg = S.ScheduleConfig(pop_size=64, generations=ARGS.island_gens, local_search="ours", seed=1)
     barrier()
     t0 = time.perf_counter()
@@ -339,6 +339,7 @@ def ga_legs(g, w, rank, world, local, barrier, dist):
     t_isl = float(tt.item())
     out["islands"] = {"islands": I * world, "generations": ARGS.island_gens, "seconds": t_isl,
                       "island_generations_per_s": I * world * ARGS.island_gens / t_isl,
+                      "mode": "one warp per island (8 per CTA), case-5, pop 64, ours",
                       "migration": "2 elites every 25 generations, global ring, NCCL all-gather"}
     return out
 

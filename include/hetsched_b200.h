@@ -91,6 +91,11 @@ typedef struct hs_ga hs_ga;
  * Generator(PCG64(seed)) state of :528).  Population and RNG stay on the
  * device between hs_ga_run calls, so a run can be cut into epochs. */
 int hs_ga_create(hs_instance *h, const hs_ga_config *cfg, int islands, const hs_pcg64 *rng, hs_ga **out);
+/* mode 0: one CTA per island (all warps price each generation's snapshots in
+ * parallel; lowest single-island latency).  mode 1: one warp per island
+ * (d_pp <= 8; up to 8 islands per CTA sharing the staged tables; highest
+ * island throughput).  Results are identical in both modes. */
+int hs_ga_create_ex(hs_instance *h, const hs_ga_config *cfg, int islands, const hs_pcg64 *rng, int mode, hs_ga **out);
 /* advance every island to generation `until` (or its patience stop) */
 int hs_ga_run(hs_ga *ga, int until, void *stream);
 /* island migration (no reference counterpart): export each

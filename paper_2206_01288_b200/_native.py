@@ -102,6 +102,7 @@ def lib():
         L.hs_path_batch.argtypes = [vp, i32, i64, vp, vp, i32, vp]
         pcg = C.POINTER(PCG64)
         L.hs_ga_create.argtypes = [vp, C.POINTER(GAConfig), i32, pcg, C.POINTER(vp)]
+        L.hs_ga_create_ex.argtypes = [vp, C.POINTER(GAConfig), i32, pcg, i32, C.POINTER(vp)]
         L.hs_ga_run.argtypes = [vp, i32, vp]
         L.hs_ga_export.argtypes = [vp, i32, vp, vp, vp]
         L.hs_ga_import.argtypes = [vp, i32, vp, vp, vp, vp]
@@ -123,7 +124,7 @@ def lib():
 
 
 EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_destroy", "hs_instance_tables",
-           "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_run",
+           "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
            "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
            "hs_random_assignments")
@@ -185,8 +186,9 @@ class Instance:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and _lib is not None:
-            _lib.hs_instance_destroy(h)
+        lib = globals().get("_lib")
+        if h is not None and lib is not None:
+            lib.hs_instance_destroy(h)
             self.handle = None
 
     def tables(self):

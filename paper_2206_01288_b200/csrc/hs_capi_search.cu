@@ -80,6 +80,7 @@ static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
     a.hk = h->hk;
     a.pop = ga->cfg.pop_size;
     a.generations = ga->cfg.generations;
+    a.islands = ga->islands;
     a.kind = ga->cfg.kind;
     a.max_passes = ga->cfg.max_passes;
     a.patience = ga->cfg.patience;
@@ -105,6 +106,11 @@ static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
 extern "C" {
 
 int hs_ga_create(hs_instance* h, const hs_ga_config* cfg, int islands, const hs_pcg64* rng, hs_ga** out) {
+    return hs_ga_create_ex(h, cfg, islands, rng, 0, out);
+}
+
+int hs_ga_create_ex(hs_instance* h, const hs_ga_config* cfg, int islands, const hs_pcg64* rng, int mode,
+                    hs_ga** out) {
     if (!h || !cfg || !rng || !out) return fail(-2, "null argument");
     if (islands < 1) return fail(-2, "islands must be >= 1");
     if (cfg->pop_size < 2) return fail(-2, "pop_size must be >= 2");
@@ -117,7 +123,7 @@ int hs_ga_create(hs_instance* h, const hs_ga_config* cfg, int islands, const hs_
     ga->h = h;
     ga->cfg = *cfg;
     ga->islands = islands;
-    if (hs::search_plan(shape_of(h, cfg->max_passes), cfg->pop_size, h->smem_optin, &ga->plan)) {
+    if (hs::search_plan(shape_of(h, cfg->max_passes), cfg->pop_size, h->smem_optin, &ga->plan, mode == 1)) {
         delete ga;
         return fail(-3, "GA working set does not fit shared memory");
     }

@@ -732,6 +732,21 @@ struct Pricer {
         }
     }
 
+    // warp-island mode: the calling warp prices one candidate with full outputs
+    __device__ void one_warp(const int16_t* cand, int lane, double* out3, double* out_pg, int8_t* out_order) const {
+        const int k = v.k;
+        double dp, pp;
+        warp_price<KeyT, kM8>(v, ws, cand, lane, dp, pp);
+        if (lane == 0) {
+            out3[0] = dp + pp;
+            out3[1] = dp;
+            out3[2] = pp;
+            if (out_order) held_karp_order(k, ws.E, ws.h, v.hk.hoff, pp, out_order);
+        }
+        if (out_pg && lane < k) out_pg[lane] = ws.pg[lane];
+        __syncwarp();
+    }
+
     // price one candidate with full outputs; every thread calls it
     __device__ void one(const int16_t* cand, int wid, int lane, double* out3, double* out_pg, int8_t* out_order) const {
         const int k = v.k;
@@ -788,11 +803,21 @@ __device__ inline Pricer<KeyT, kM8, kCta> make_pricer(int n, int k, int m, const
     return pr;
 }
 
-template <bool kSmemTables, typename KeyT, bool kM8, bool kCta>
+// kWI (warp islands): every warp of the CTA runs its own island (its own
+// working set, pricing its snapshots itself); the CTA only shares the staged
+// tables.  Otherwise one island per CTA, warp 0 drives and all warps price.
+template <bool kSmemTables, typename KeyT, bool kM8, bool kCta, bool kWI>
 __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const int isl = blockIdx.x;
+    const int isl = kWI ? blockIdx.x * W + wid : blockIdx.x;
+    auto island_sync = [&]() {
+        if constexpr (kWI)
+            __syncwarp();
+        else
+            __syncthreads();
+    };
+    const int pw = kWI ? 0 : wid, pW = kWI ? 1 : W;  // pricing lanes of this island
     const int n = a.n, k = a.k, m = kM8 ? 8 : a.m, km = k * m, P = a.pop, cap = m + 1;
     const int max_snaps = 1 + a.max_passes;
     size_t off = 0;
@@ -813,45 +838,60 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         return p;
     };
     GASmem g;
-    g.snaps = reinterpret_cast<int16_t*>(take((size_t)max_snaps * km * 2));
-    g.snapcost = reinterpret_cast<double*>(take((size_t)max_snaps * 8));
-    g.popcost = reinterpret_cast<double*>(take((size_t)P * 8));
-    g.best = reinterpret_cast<int16_t*>(take((size_t)km * 2));
-    g.par = reinterpret_cast<int16_t*>(take((size_t)2 * km * 2));
-    g.ctl = reinterpret_cast<int*>(take(16 * 4));
+    GAState* stp = nullptr;
+    auto carve = [&]() {
+        g.snaps = reinterpret_cast<int16_t*>(take((size_t)max_snaps * km * 2));
+        g.snapcost = reinterpret_cast<double*>(take((size_t)max_snaps * 8));
+        g.popcost = reinterpret_cast<double*>(take((size_t)P * 8));
+        g.best = reinterpret_cast<int16_t*>(take((size_t)km * 2));
+        g.par = reinterpret_cast<int16_t*>(take((size_t)2 * km * 2));
+        g.ctl = reinterpret_cast<int*>(take(16 * 4));
+        LS& s = g.ls;
+        s.n = n;
+        s.k = k;
+        s.m = m;
+        s.cap = cap;
+        s.W = SW;
+        s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
+        s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
+        s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
+        s.mver = reinterpret_cast<uint32_t*>(take((size_t)n * k * 4));
+        s.cver = reinterpret_cast<uint32_t*>(take((size_t)k * 4));
+        s.home = reinterpret_cast<double*>(take((size_t)n * 8));
+        s.valid = reinterpret_cast<int*>(take(16));
+        s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+        s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
+        s.nlocked = reinterpret_cast<int*>(take(4));
+        s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
+        s.f64 = reinterpret_cast<double*>(take((size_t)(4 * cap + 2 * k + 2) * 8));
+        s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
+        s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+        stp = reinterpret_cast<GAState*>(take(sizeof(GAState)));
+    };
+    if constexpr (kWI) {
+        for (int w = 0; w <= wid; w++) carve();
+    } else {
+        carve();
+    }
     LS& s = g.ls;
-    s.n = n;
-    s.k = k;
-    s.m = m;
-    s.cap = cap;
-    s.W = SW;
-    s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
-    s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
-    s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
-    s.mver = reinterpret_cast<uint32_t*>(take((size_t)n * k * 4));
-    s.cver = reinterpret_cast<uint32_t*>(take((size_t)k * 4));
-    for (int t = threadIdx.x; t < n * k; t += blockDim.x) s.mver[t] = 0;
-    for (int t = threadIdx.x; t < k; t += blockDim.x) s.cver[t] = 1;
-    s.home = reinterpret_cast<double*>(take((size_t)n * 8));
-    s.valid = reinterpret_cast<int*>(take(16));
-    s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
-    s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
-    s.nlocked = reinterpret_cast<int*>(take(4));
-    s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
-    s.f64 = reinterpret_cast<double*>(take((size_t)(4 * cap + 2 * k + 2) * 8));
-    s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
-    s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+    {
+        const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+        for (int t = t0; t < n * k; t += dt) s.mver[t] = 0;
+        for (int t = t0; t < k; t += dt) s.cver[t] = 1;
+    }
     __syncthreads();
+    if (kWI && isl >= a.islands) return;  // no block-wide syncs below in warp-island mode
 
-    __shared__ GAState st;
-    if (threadIdx.x == 0) st = a.state[isl];
-    __syncthreads();
+    GAState& st = *stp;
+    if ((kWI ? lane : threadIdx.x) == 0) st = a.state[isl];
+    island_sync();
+
     int16_t* pop = a.pop_buf + (size_t)isl * P * km;
     double* gcost = a.cost_buf + (size_t)isl * P;
     int16_t* gbest = a.best_buf + (size_t)isl * km;
     Pcg64 rng;
-    if (wid == 0) rng.load(st.rng);
-    const bool driver = wid == 0;
+    const bool driver = kWI || wid == 0;
+    if (driver) rng.load(st.rng);
     if (a.prof && isl == 0 && threadIdx.x == 0) g_prof = a.prof;
 
     if (!st.initialized) {
@@ -888,14 +928,15 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             }
         }
         __threadfence_block();
-        __syncthreads();
+        island_sync();
         // price the population in chunks of max_snaps through smem
         for (int c0 = 0; c0 < P; c0 += max_snaps) {
             int cnt = min(max_snaps, P - c0);
-            for (int t = threadIdx.x; t < cnt * km; t += blockDim.x) g.snaps[t] = pop[(size_t)c0 * km + t];
-            __syncthreads();
-            pr.all(g.snaps, cnt, km, g.popcost + c0, wid, W, lane);
-            __syncthreads();
+            const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+            for (int t = t0; t < cnt * km; t += dt) g.snaps[t] = pop[(size_t)c0 * km + t];
+            island_sync();
+            pr.all(g.snaps, cnt, km, g.popcost + c0, pw, pW, lane);
+            island_sync();
         }
         if (driver) {
             if (lane == 0) {
@@ -914,14 +955,15 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             copy16(gbest, pop + (size_t)st.best_idx * km, km, lane);
         }
     } else {
-        for (int t = threadIdx.x; t < P; t += blockDim.x) g.popcost[t] = gcost[t];
+        const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+        for (int t = t0; t < P; t += dt) g.popcost[t] = gcost[t];
     }
     if (driver && lane == 0) {
         g.ctl[1] = st.stopped;
         g.ctl[2] = st.gen;
     }
     __threadfence_block();
-    __syncthreads();
+    island_sync();
 
     const int gen_end = min(a.gen_end, a.generations);
     const int stop_after = a.kind == 0 ? 2 : 1;
@@ -969,11 +1011,11 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             if (lane == 0) g.ctl[0] = nsnap;
         }
         long long q0 = clock64();
-        __syncthreads();
+        island_sync();
         const int nsnap = g.ctl[0];
-        pr.all(g.snaps, nsnap, km, g.snapcost, wid, W, lane);
-        __syncthreads();
-        if (a.prof && isl == 0 && threadIdx.x == 0) a.prof[3] += clock64() - q0;
+        pr.all(g.snaps, nsnap, km, g.snapcost, pw, pW, lane);
+        island_sync();
+        if (a.prof && isl == 0 && lane == 0 && driver) a.prof[3] += clock64() - q0;
         if (driver) {
             int bsi = 0, worst = 0, replace = 0, improve = 0;
             double cb = 0.0;
@@ -1014,11 +1056,14 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             }
         }
         __threadfence_block();
-        __syncthreads();
+        island_sync();
     }
 
     // persist population costs; finalize when the run is over
-    for (int t = threadIdx.x; t < P; t += blockDim.x) gcost[t] = g.popcost[t];
+    {
+        const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+        for (int t = t0; t < P; t += dt) gcost[t] = g.popcost[t];
+    }
     bool finished = g.ctl[1] || g.ctl[2] >= a.generations;
     if (finished && a.finalize && !st.finalized) {
         // canonical() (costmodel.py:86-88) then a last priced evaluation (:572-574)
@@ -1036,9 +1081,13 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             for (int j = 0; j < k; j++)
                 for (int i = 0; i < m; i++) g.snaps[j * m + i] = gbest[ord[j] * m + i];
         }
-        __syncthreads();
-        pr.one(g.snaps, wid, lane, a.out3 + isl * 3, a.out_pg ? a.out_pg + (size_t)isl * k : nullptr,
-               a.out_order ? a.out_order + (size_t)isl * k : nullptr);
+        island_sync();
+        if constexpr (kWI)
+            pr.one_warp(g.snaps, lane, a.out3 + isl * 3, a.out_pg ? a.out_pg + (size_t)isl * k : nullptr,
+                        a.out_order ? a.out_order + (size_t)isl * k : nullptr);
+        else
+            pr.one(g.snaps, wid, lane, a.out3 + isl * 3, a.out_pg ? a.out_pg + (size_t)isl * k : nullptr,
+                   a.out_order ? a.out_order + (size_t)isl * k : nullptr);
         if (driver) {
             copy16(a.out_groups + (size_t)isl * km, g.snaps, km, lane);
             if (lane == 0) {
@@ -1047,7 +1096,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             }
         }
     }
-    __syncthreads();
+    island_sync();
     if (driver && lane == 0) {
         rng.store(st.rng);
         a.state[isl] = st;
@@ -1245,23 +1294,24 @@ static size_t ls_bytes(int n, int k, int m) {
            al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
 }
 
-static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P) {
+static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P, bool warp_islands = false) {
     auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
     ScratchLayout wl = scratch_layout(sh.k <= 8 ? sh.k : 8, sh.m);
     int km = sh.k * sh.m, ms = 1 + sh.max_passes;
     size_t b = sh.k <= 8 ? hk_smem_bytes(sh.hk) + (size_t)W * wl.bytes : al(cta_scratch_bytes(sh.k, sh.m));
     if (smem_tables)
         b += (size_t)sh.n * sh.n * 8 + al((size_t)sh.n * sh.n * (sh.key16 ? 2 : 4)) + (size_t)sh.n * sh.n * 8;
-    b += al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) + al((size_t)2 * km * 2) +
-         al(64);
-    b += ls_bytes(sh.n, sh.k, sh.m);
+    size_t isl = al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) +
+                 al((size_t)2 * km * 2) + al(64) + ls_bytes(sh.n, sh.k, sh.m) + al(sizeof(GAState));
+    b += (warp_islands ? (size_t)W : 1) * isl;
     return b;
 }
 
-int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan) {
+int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan, bool warp_islands) {
+    plan->warp_islands = warp_islands && sh.k <= 8;
     for (int W : {8, 6, 4, 2, 1}) {
         for (int st = 1; st >= 0; st--) {
-            size_t b = ga_bytes(sh, W, st, P);
+            size_t b = ga_bytes(sh, W, st, P, plan->warp_islands);
             if (b <= smem_optin) {
                 plan->warps = W;
                 plan->smem_tables = st;
@@ -1278,8 +1328,17 @@ int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* pla
 template <bool S, typename KT, bool M8, bool CT>
 static int launch_ga_t(const GAArgs& a, const SearchPlan& plan, int islands, cudaStream_t st) {
     ScratchLayout wl = scratch_layout(a.k <= 8 ? a.k : 8, a.m);
-    cudaFuncSetAttribute(ga_kernel<S, KT, M8, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-    ga_kernel<S, KT, M8, CT><<<islands, plan.warps * 32, plan.smem, st>>>(a, wl);
+    if constexpr (!CT) {
+        if (plan.warp_islands) {
+            cudaFuncSetAttribute(ga_kernel<S, KT, M8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)plan.smem);
+            int blocks = (islands + plan.warps - 1) / plan.warps;
+            ga_kernel<S, KT, M8, false, true><<<blocks, plan.warps * 32, plan.smem, st>>>(a, wl);
+            return cudaGetLastError() == cudaSuccess ? 0 : -1;
+        }
+    }
+    cudaFuncSetAttribute(ga_kernel<S, KT, M8, CT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
+    ga_kernel<S, KT, M8, CT, false><<<islands, plan.warps * 32, plan.smem, st>>>(a, wl);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

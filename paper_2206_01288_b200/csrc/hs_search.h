@@ -24,6 +24,7 @@ struct GAArgs {
     const double* vals;
     HKTables hk;
     int pop, generations, kind /*0 ours 1 kl 2 none*/, max_passes, patience /*<=0: none*/;
+    int islands;
     HKBig hkb;            // d_pp > 8: CTA pricing schedule
     double* hk_scratch;   // d_pp > 8: per-island Held-Karp slices
     size_t hk_size;
@@ -69,11 +70,11 @@ struct SearchShape {
 
 struct SearchPlan {
     int warps;
-    bool smem_tables, m8, cta;
+    bool smem_tables, m8, cta, warp_islands;
     size_t smem;
 };
 
-int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan);
+int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan, bool warp_islands = false);
 int launch_ga(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st);
 int launch_refine(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st);
 int launch_crossover(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs, int16_t* out, int B,

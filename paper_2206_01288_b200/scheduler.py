@@ -244,7 +244,9 @@ def local_search(g, w, p, kind: str = "ours", rng: np.random.Generator | None = 
 class GASession:
     """Islands of independent steady-state GAs on one GPU (hs_ga_* C-ABI)."""
 
-    def __init__(self, g, w, cfg: ScheduleConfig, rngs, device: int | None = None):
+    def __init__(self, g, w, cfg: ScheduleConfig, rngs, device: int | None = None, mode: str = "cta"):
+        """mode "cta": one CTA per island (lowest latency); "warp": one warp per
+        island (throughput; d_pp <= 8).  Both give identical results."""
         validate_workload(w, g.lat.shape[0])
         if cfg.local_search == "ours" and w.d_pp == 1 and w.d_dp >= 2:
             raise ValueError("zero-size array to reduction operation maximum which has no identity")
@@ -257,13 +259,15 @@ class GASession:
                                cfg.patience or 0)
         st = _states(self.rngs)
         h = C.c_void_p()
-        N.check(L.hs_ga_create(self.inst.handle, C.byref(self._cfg), self.islands, st, C.byref(h)), "hs_ga_create")
+        N.check(L.hs_ga_create_ex(self.inst.handle, C.byref(self._cfg), self.islands, st,
+                                  1 if mode == "warp" else 0, C.byref(h)), "hs_ga_create_ex")
         self.handle = h
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and N._lib is not None:
-            N._lib.hs_ga_destroy(h)
+        lib = getattr(N, "_lib", None) if N is not None else None
+        if h is not None and lib is not None:
+            lib.hs_ga_destroy(h)
             self.handle = None
 
     @property
@@ -371,7 +375,7 @@ def gather_elites(groups, costs, group=None):
 
 
 def evolve_islands(g, w, cfg: ScheduleConfig, islands_per_rank: int, migrate_every: int = 0, elites: int = 2,
-                   group=None) -> list[ScheduleResult]:
+                   group=None, mode: str = "warp") -> list[ScheduleResult]:
     """Run islands_per_rank GA instances on this rank's GPU, streams from
     SeedSequence(cfg.seed).spawn(world * islands_per_rank); every
     `migrate_every` generations (0 = never) each island sends its `elites`
@@ -382,7 +386,7 @@ def evolve_islands(g, w, cfg: ScheduleConfig, islands_per_rank: int, migrate_eve
     world = dist.get_world_size(group) if dist_on else 1
     I = int(islands_per_rank)
     rngs = island_seeds(cfg.seed, I, offset=rank * I)
-    sess = GASession(g, w, cfg, rngs)
+    sess = GASession(g, w, cfg, rngs, mode=mode if w.d_pp <= 8 else "cta")
     src = migration_sources(rank, world, I)
     gen = 0
     while gen < cfg.generations:

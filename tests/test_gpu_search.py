@@ -241,3 +241,16 @@ def test_local_search_d_pp_16_vs_oracle():
             out = S.local_search(g, w, p, kind=kind, rng=r1)
             want = O.Oracle.of(g, w).local_search(np.array(p.groups, dtype=np.int32), kind, st)
             assert [list(x) for x in out.groups] == want.tolist()
+
+
+@pytest.mark.parametrize("kind", ["ours", "kl", "none"])
+def test_warp_island_mode_equals_cta_mode(kind):
+    """One warp per island gives the same results as one CTA per island."""
+    g, w = I.instance("case5")
+    cfg = S.ScheduleConfig(pop_size=16, generations=20, local_search=kind)
+    a = S.GASession(g, w, cfg, S.island_seeds(3, 37), mode="cta")
+    b = S.GASession(g, w, cfg, S.island_seeds(3, 37), mode="warp")
+    a.run(cfg.generations)
+    b.run(cfg.generations)
+    ra, rb = a.results(), b.results()
+    assert [r.to_dict() for r in ra] == [r.to_dict() for r in rb]
