@@ -59,6 +59,13 @@ int hs_instance_tables(hs_instance *h, double *dp, double *pp, double *sw);
 int hs_eval_batch(hs_instance *h, const int16_t *groups, int64_t P, double *total, double *datap,
                   double *pipelinep, double *per_group, int8_t *order, int32_t *invalid, void *stream);
 
+/* hs_eval_batch with heuristic=True semantics (comm_cost(..., heuristic=True),
+ * costmodel.py:217): d_pp > 16 orders stages with nearest-neighbour + 2-opt
+ * (combinatorics.py:299-342) instead of exact Held-Karp; d_pp <= 16 is
+ * exact either way.  Partitions are not validated here (callers do). */
+int hs_eval_batch_ex(hs_instance *h, const int16_t *groups, int64_t P, double *total, double *datap, double *pipelinep,
+                     double *per_group, int8_t *order, int32_t *invalid, int heuristic, void *stream);
+
 /* Same, host buffers (pinned for full overlap); copies in, evaluates in
  * double-buffered chunks, copies out, returns when done.  *invalid (host)
  * receives the malformed-candidate count. */
@@ -68,6 +75,11 @@ int hs_eval_batch_host(hs_instance *h, const int16_t *groups, int64_t P, double 
 /* bottleneck_value (combinatorics.py:128-131) of B matrices [B][m][m],
  * m <= 64, entries finite and >= 0 (device pointers). */
 int hs_bottleneck_batch(const double *w, int m, int64_t B, double *out, int device, void *stream);
+
+/* open_loop_tsp(heuristic=True) for any 2 <= k <= 64: nearest neighbour from
+ * every start + first-improvement 2-opt (combinatorics.py:299-342); device
+ * pointers, one thread per matrix. */
+int hs_path_heuristic_batch(const double *w, int k, int64_t B, double *total, int8_t *order, int device, void *stream);
 
 /* exact open_loop_tsp (combinatorics.py:232-296, Held-Karp) of B symmetric
  * [B][k][k] matrices, k <= 8: total [B] and lexicographically smallest

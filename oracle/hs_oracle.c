@@ -433,6 +433,29 @@ int orc_comm_cost(const orc_inst *in, const int32_t *groups, double *out3, doubl
     return 0;
 }
 
+/* comm_cost(..., heuristic=True) (costmodel.py:217-229): exact Held-Karp up
+ * to 16 stages, nearest neighbour + 2-opt beyond (combinatorics.py:243-249) */
+int orc_comm_cost_heuristic(const orc_inst *in, const int32_t *groups, double *out3, int32_t *order) {
+    int k = in->k, m = in->m;
+    if (k <= MAX_EXACT_TSP) return orc_comm_cost(in, groups, out3, NULL, order);
+    double datap = 0.0;
+    for (int j = 0; j < k; j++) {
+        double v = orc_datap_group(in, groups + j * m, m);
+        if (j == 0 || v > datap) datap = v;
+    }
+    double *E = (double *)malloc(sizeof(double) * k * k);
+    coarse_edges(in, groups, E);
+    double pipe;
+    int32_t ord[256];
+    orc_open_loop_tsp_heuristic(E, k, &pipe, ord);
+    free(E);
+    out3[0] = datap + pipe;
+    out3[1] = datap;
+    out3[2] = pipe;
+    if (order) memcpy(order, ord, sizeof(int32_t) * k);
+    return 0;
+}
+
 typedef struct {
     const orc_inst *in;
     const int16_t *groups;

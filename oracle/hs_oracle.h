@@ -38,6 +38,7 @@ void orc_tables(const orc_inst *in, double *dp, double *pp, double *sw);
 /* one partition: groups[k*m], members ascending.  order may be NULL. */
 int orc_comm_cost(const orc_inst *in, const int32_t *groups, double *out3,
                   double *per_group, int32_t *order);
+int orc_comm_cost_heuristic(const orc_inst *in, const int32_t *groups, double *out3, int32_t *order);
 /* batch over int16 [P][k][m]; nthreads <= 0 -> 1 */
 int orc_comm_cost_batch(const orc_inst *in, const int16_t *groups, int64_t P,
                         double *total, double *datap, double *pipelinep, int nthreads);

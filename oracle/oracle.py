@@ -72,6 +72,7 @@ def lib():
         L.orc_destroy.argtypes = [C.c_void_p]
         L.orc_tables.argtypes = [C.c_void_p, _f64p, _f64p, _f64p]
         L.orc_comm_cost.argtypes = [C.c_void_p, _i32p, _f64p, _f64p, _i32p]
+        L.orc_comm_cost_heuristic.argtypes = [C.c_void_p, _i32p, _f64p, _i32p]
         L.orc_comm_cost_batch.argtypes = [C.c_void_p, _i16p, C.c_int64, _f64p, _f64p, _f64p, C.c_int]
         L.orc_bottleneck_value.restype = C.c_double
         L.orc_bottleneck_value.argtypes = [_f64p, C.c_int]
@@ -148,6 +149,14 @@ class Oracle:
         if rc:
             raise ValueError(f"oracle comm_cost failed rc={rc}")
         return o3[0], o3[1], o3[2], pg, order
+
+    def comm_cost_heuristic(self, groups):
+        g = np.ascontiguousarray(groups, dtype=np.int32).reshape(self.k, self.m)
+        o3 = np.empty(3)
+        order = np.empty(self.k, dtype=np.int32)
+        if lib().orc_comm_cost_heuristic(self._h, g, o3, order):
+            raise ValueError("oracle heuristic comm_cost failed")
+        return o3[0], o3[1], o3[2], order
 
     def comm_cost_batch(self, parts, threads=1):
         parts = np.ascontiguousarray(parts, dtype=np.int16)

@@ -98,6 +98,8 @@ def lib():
         L.hs_instance_tables.argtypes = [vp, vp, vp, vp]
         L.hs_eval_batch.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]
         L.hs_eval_batch_host.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp]
+        L.hs_eval_batch_ex.argtypes = [vp, vp, i64, vp, vp, vp, vp, vp, vp, i32, vp]
+        L.hs_path_heuristic_batch.argtypes = [vp, i32, i64, vp, vp, i32, vp]
         L.hs_bottleneck_batch.argtypes = [vp, i32, i64, vp, i32, vp]
         L.hs_path_batch.argtypes = [vp, i32, i64, vp, vp, i32, vp]
         pcg = C.POINTER(PCG64)
@@ -124,7 +126,7 @@ def lib():
 
 
 EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_destroy", "hs_instance_tables",
-           "hs_eval_batch", "hs_eval_batch_host", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
+           "hs_eval_batch", "hs_eval_batch_ex", "hs_eval_batch_host", "hs_path_heuristic_batch", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
            "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
            "hs_random_assignments")

@@ -104,6 +104,21 @@ def open_loop_tsps(stack) -> tuple[np.ndarray, np.ndarray]:
     return tot.cpu().numpy(), order.cpu().numpy().astype(np.int64)
 
 
+def heuristic_paths(stack) -> tuple[np.ndarray, np.ndarray]:
+    """Nearest neighbour + 2-opt (combinatorics.py:299-342) on a [B, k, k]
+    stack, k <= 64, one GPU thread per matrix."""
+    a = np.ascontiguousarray(stack, dtype=np.float64)
+    B, k = a.shape[0], a.shape[1]
+    torch = N.torch_cuda()
+    dev = N.current_device()
+    w = torch.from_numpy(a).to(f"cuda:{dev}")
+    tot = torch.empty(B, dtype=torch.float64, device=f"cuda:{dev}")
+    order = torch.empty((B, k), dtype=torch.int8, device=f"cuda:{dev}")
+    N.check(N.lib().hs_path_heuristic_batch(w.data_ptr(), k, B, tot.data_ptr(), order.data_ptr(), dev,
+                                            N.stream_ptr(dev)), "hs_path_heuristic_batch")
+    return tot.cpu().numpy(), order.cpu().numpy().astype(np.int64)
+
+
 def open_loop_tsp(weights, heuristic: bool = False) -> PathResult:
     """Minimum-cost Hamiltonian path, endpoints free (exact up to 16 vertices)."""
     w = _checked_symmetric(weights)
@@ -115,6 +130,7 @@ def open_loop_tsp(weights, heuristic: bool = False) -> PathResult:
             raise ValueError(
                 f"exact path search is limited to {MAX_EXACT_TSP} vertices, got {k}; "
                 "pass heuristic=True to accept an approximate tour")
-        raise NotImplementedError("the NN+2-opt heuristic (k > 16) is not on the GPU path yet")
+        tot, order = heuristic_paths(w[None])
+        return PathResult(tuple(int(x) for x in order[0]), float(tot[0]))
     tot, order = open_loop_tsps(w[None])
     return PathResult(tuple(int(x) for x in order[0]), float(tot[0]))

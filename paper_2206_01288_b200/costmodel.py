@@ -99,7 +99,8 @@ def _check_partition(p, g, w) -> None:
             f"partition shape {len(p.groups)}x{len(p.groups[0])} does not match workload {w.d_pp}x{w.d_dp}")
 
 
-def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = False, device: int | None = None):
+def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = False, device: int | None = None,
+                    heuristic: bool = False):
     """Costs of a batch of partitions in one GPU pass.
 
     ``groups``: int16-compatible [P, d_pp, d_dp] with ascending members --
@@ -110,6 +111,11 @@ def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = Fals
     Malformed partitions raise CostModelError.
     """
     validate_workload(w, g.lat.shape[0])
+    if w.d_pp > 16:
+        if not heuristic:
+            raise ValueError(f"exact path search is limited to 16 vertices, got {w.d_pp}; "
+                             "pass heuristic=True to accept an approximate tour")
+        return _comm_cost_batch_heuristic(g, groups, w, per_group, order, device)
     inst = N.instance_for(g, w, device)
     k = inst.k
     if isinstance(groups, np.ndarray) or not hasattr(groups, "data_ptr"):
@@ -153,11 +159,41 @@ def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = Fals
     return out
 
 
+def _comm_cost_batch_heuristic(g, groups, w, per_group, order, device):
+    """d_pp > 16 with heuristic=True: NN + 2-opt stage order on the GPU."""
+    a = np.ascontiguousarray(groups, dtype=np.int16)
+    k, m = w.d_pp, w.d_dp
+    if a.ndim != 3 or a.shape[1:] != (k, m):
+        raise CostModelError(f"expected groups of shape [P, {k}, {m}], got {a.shape}")
+    srt = np.sort(a.reshape(a.shape[0], -1), axis=1)
+    if a.shape[0] and not (np.array_equal(srt, np.broadcast_to(np.arange(k * m), srt.shape))
+                           and np.all(np.diff(a, axis=2) > 0)):
+        raise CostModelError("partitions must cover 0..N-1 with ascending members")
+    inst = N.instance_for(g, w, device)
+    torch = N.torch_cuda()
+    dev = f"cuda:{inst.device}"
+    P = a.shape[0]
+    t = torch.from_numpy(a).to(dev)
+    out = {name: torch.empty(P, dtype=torch.float64, device=dev) for name in ("total", "datap", "pipelinep")}
+    out["per_group"] = torch.empty((P, k), dtype=torch.float64, device=dev)
+    out["order"] = torch.empty((P, k), dtype=torch.int8, device=dev)
+    N.check(N.lib().hs_eval_batch_ex(inst.handle, t.data_ptr(), P, out["total"].data_ptr(), out["datap"].data_ptr(),
+                                     out["pipelinep"].data_ptr(), out["per_group"].data_ptr(),
+                                     out["order"].data_ptr(), None, 1, N.stream_ptr(inst.device)), "hs_eval_batch_ex")
+    res = {key: val.cpu().numpy() for key, val in out.items()}
+    if not per_group:
+        res.pop("per_group")
+    if not order:
+        res.pop("order")
+    return res
+
+
 def comm_cost(g, p, w, heuristic: bool = False) -> CostBreakdown:
     """Full bi-level cost of one balanced partition (costmodel.py:217-229)."""
     validate_workload(w, g.lat.shape[0])
     _check_partition(p, g, w)
-    r = comm_cost_batch(g, np.asarray([p.groups], dtype=np.int16), w, per_group=True, order=True)
+    r = comm_cost_batch(g, np.asarray([p.groups], dtype=np.int16), w, per_group=True, order=True,
+                        heuristic=heuristic)
     total, datap, pipe = float(r["total"][0]), float(r["datap"][0]), float(r["pipelinep"][0])
     return CostBreakdown(datap=datap, pipelinep=pipe, total=total,
                          per_group_datap=tuple(float(x) for x in r["per_group"][0]),

@@ -120,3 +120,96 @@ int launch_path_cta(const double* w, int k, int64_t B, const HKBig& t, double* s
 }
 
 }  // namespace hs
+
+namespace hs {
+
+// open_loop_tsp(heuristic=True), one thread per matrix (any k <= 64)
+__global__ void path_heuristic_kernel(const double* __restrict__ w, int k, int64_t B, double* __restrict__ total,
+                                      int8_t* __restrict__ order, int8_t* __restrict__ scratch) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    int8_t* best = scratch + b * 2 * k;
+    int8_t* o = best + k;
+    total[b] = nn_two_opt(w + b * k * k, k, k, best, o);
+    if (order)
+        for (int i = 0; i < k; i++) order[b * k + i] = best[i];
+}
+
+int launch_path_heuristic(const double* w, int k, int64_t B, double* total, int8_t* order, int8_t* scratch,
+                          cudaStream_t s) {
+    if (B == 0) return 0;
+    path_heuristic_kernel<<<(unsigned)((B + 63) / 64), 64, 0, s>>>(w, k, B, total, order, scratch);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// comm_cost(heuristic=True) for 16 < d_pp <= 64: one CTA per candidate,
+// datap rows and bottleneck edges in parallel, heuristic path on thread 0.
+template <typename KeyT>
+__global__ void __launch_bounds__(256) eval_heur_kernel(EvalArgs a, double* Ebuf) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int k = a.k, m = a.m, km = k * m, n = a.n, es = k;
+    double* rows = reinterpret_cast<double*>(smem);
+    double* pg = rows + km;
+    int16_t* mem = reinterpret_cast<int16_t*>(pg + 64);
+    int8_t* ord = reinterpret_cast<int8_t*>(mem + km + 8);
+    double* E = Ebuf + (size_t)blockIdx.x * k * k;
+    const KeyT* RK = reinterpret_cast<const KeyT*>(a.rank);
+    for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
+        for (int i = threadIdx.x; i < km; i += blockDim.x) mem[i] = a.groups[p * km + i];
+        __syncthreads();
+        for (int r = threadIdx.x; r < km; r += blockDim.x) {
+            int g = r / m;
+            const int16_t* gm = mem + g * m;
+            const double* row = a.dp + (size_t)gm[r - g * m] * n;
+            rows[r] = pairwise_sum(m, [&](int c) { return row[gm[c]]; });
+        }
+        __syncthreads();
+        if (threadIdx.x < k) {
+            double mx = rows[threadIdx.x * m];
+            for (int i = 1; i < m; i++) mx = dmax(mx, rows[threadIdx.x * m + i]);
+            pg[threadIdx.x] = mx;
+        }
+        const int npairs = k * (k - 1) / 2;
+        for (int t = threadIdx.x; t < npairs; t += blockDim.x) {
+            int j, j2;
+            decode_pair(t, k, j, j2);
+            const int16_t* A = mem + j * m;
+            const int16_t* Bg = mem + j2 * m;
+            uint32_t L = bottleneck_threshold<uint32_t>(
+                m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * n + Bg[c]]; }, 0xffffffffu);
+            double v = a.vals[L];
+            E[j * es + j2] = v;
+            E[j2 * es + j] = v;
+        }
+        if (threadIdx.x < k) E[threadIdx.x * es + threadIdx.x] = 0.0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double pipe = nn_two_opt(E, es, k, ord, ord + 64);
+            double dp = pg[0];
+            for (int g = 1; g < k; g++) dp = dmax(dp, pg[g]);
+            a.total[p] = dp + pipe;
+            if (a.datap) a.datap[p] = dp;
+            if (a.pipe) a.pipe[p] = pipe;
+            if (a.order)
+                for (int i = 0; i < k; i++) a.order[p * k + i] = ord[i];
+        }
+        if (a.per_group && threadIdx.x < k) a.per_group[p * k + threadIdx.x] = pg[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+int launch_eval_heur(const EvalArgs& a, double* Ebuf, int blocks, cudaStream_t s) {
+    if (a.P == 0) return 0;
+    blocks = (int)std::min<int64_t>(blocks, a.P);
+    size_t smem = (size_t)a.k * a.m * 8 + 64 * 8 + ((size_t)a.k * a.m + 8) * 2 + 160;
+    if (a.key16) {
+        cudaFuncSetAttribute(eval_heur_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        eval_heur_kernel<uint16_t><<<blocks, 256, smem, s>>>(a, Ebuf);
+    } else {
+        cudaFuncSetAttribute(eval_heur_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        eval_heur_kernel<uint32_t><<<blocks, 256, smem, s>>>(a, Ebuf);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace hs

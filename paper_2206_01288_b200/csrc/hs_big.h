@@ -13,4 +13,8 @@ int launch_eval_cta(const EvalArgs& a, const HKBig& t, double* scratch, int bloc
 int launch_path_cta(const double* w, int k, int64_t B, const HKBig& t, double* scratch, int blocks, double* total,
                     int8_t* order, cudaStream_t s);
 
+int launch_path_heuristic(const double* w, int k, int64_t B, double* total, int8_t* order, int8_t* scratch,
+                          cudaStream_t s);
+int launch_eval_heur(const EvalArgs& a, double* Ebuf, int blocks, cudaStream_t s);
+
 }  // namespace hs

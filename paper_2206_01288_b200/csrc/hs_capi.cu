@@ -166,6 +166,7 @@ static hs::EvalArgs base_args(const hs_instance* h) {
 }
 
 static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
+    if (h->k > 16) return hsx::fail(-3, "exact pricing is limited to d_pp <= 16 (Held-Karp); use heuristic paths");
     if (h->k > hs::kWarpK)
         return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
                                    a.key16 && a.m == 8 && a.nvals <= 0x8000, s);
@@ -183,7 +184,7 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
     if (!out || !lat || !bw) return fail(-2, "null argument");
     if (n < 1 || d_pp < 1 || d_dp < 1 || (int64_t)d_pp * d_dp != n) return fail(-2, "d_pp*d_dp must equal n");
     if (d_dp > hs::kMaxM) return fail(-3, "d_dp > 64 is not supported");
-    if (d_pp > 16) return fail(-3, "d_pp > 16 needs the heuristic path search (exact Held-Karp is limited to 16)");
+    if (d_pp > 64) return fail(-3, "d_pp > 64 is not supported");
     if (n > 32767) return fail(-3, "n > 32767 is not supported (int16 device ids)");
     DeviceGuard dg(device);
     hs_instance* h = new hs_instance();
@@ -225,7 +226,12 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
     CK(cudaDeviceSynchronize(), "instance tables");
     int rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk);
     if (rc) return rc;
-    if (d_pp > hs::kWarpK) {
+    if (d_pp > 16) {
+        // exact pricing is limited to 16 stages (combinatorics.py:243-249);
+        // such instances serve the heuristic and pass-only entry points
+        h->big_blocks = 2 * h->sm_count;
+        CK(cudaMalloc(&h->heur_E, (size_t)h->big_blocks * d_pp * d_pp * 8), "cudaMalloc heuristic E");
+    } else if (d_pp > hs::kWarpK) {
         rc = get_hk_big(device, d_pp, &h->hkb);
         if (rc) return rc;
         h->big_blocks = hs::big_blocks(h->sm_count, d_pp);
@@ -252,6 +258,7 @@ int hs_instance_destroy(hs_instance* h) {
     if (h->rank16) cudaFree(h->rank16);
     for (int i = 0; i < 2; i++)
         if (h->big_scratch[i]) cudaFree(h->big_scratch[i]);
+    if (h->heur_E) cudaFree(h->heur_E);
     cudaFree(h->invalid);
     for (int i = 0; i < 2; i++) {
         if (h->cg[i]) cudaFree(h->cg[i]);
@@ -290,6 +297,41 @@ int hs_eval_batch(hs_instance* h, const int16_t* groups, int64_t P, double* tota
     a.order = order;
     a.invalid = invalid ? invalid : h->invalid;
     if (launch_any(h, a, 0, (cudaStream_t)stream)) return fail(-1, "eval launch", cudaGetLastError());
+    return 0;
+}
+
+int hs_eval_batch_ex(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap, double* pipelinep,
+                     double* per_group, int8_t* order, int32_t* invalid, int heuristic, void* stream) {
+    if (!h) return fail(-2, "null handle");
+    if (h->k <= 16 || !heuristic)
+        return hs_eval_batch(h, groups, P, total, datap, pipelinep, per_group, order, invalid, stream);
+    if (P < 0) return fail(-2, "negative batch");
+    if (P == 0) return 0;
+    DeviceGuard dg(h->device);
+    hs::EvalArgs a = base_args(h);
+    a.groups = groups;
+    a.P = P;
+    a.total = total;
+    a.datap = datap;
+    a.pipe = pipelinep;
+    a.per_group = per_group;
+    a.order = order;
+    a.invalid = invalid ? invalid : h->invalid;
+    if (hs::launch_eval_heur(a, h->heur_E, h->big_blocks, (cudaStream_t)stream))
+        return fail(-1, "heuristic eval launch", cudaGetLastError());
+    return 0;
+}
+
+int hs_path_heuristic_batch(const double* w, int k, int64_t B, double* total, int8_t* order, int device, void* stream) {
+    if (k < 2 || k > 64) return fail(-3, "heuristic path: k must be in 2..64");
+    if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
+    DeviceGuard dg(device);
+    int8_t* scratch = nullptr;
+    CK(cudaMalloc(&scratch, (size_t)B * 2 * k), "cudaMalloc");
+    int rc = hs::launch_path_heuristic(w, k, B, total, order, scratch, (cudaStream_t)stream);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(scratch);
+    if (rc || e != cudaSuccess) return fail(-1, "heuristic path launch", e);
     return 0;
 }
 

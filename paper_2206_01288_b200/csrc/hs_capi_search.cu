@@ -299,7 +299,47 @@ int hs_local_search(hs_instance* h, int kind, int max_passes, int B, const int16
 
 int hs_refine_pass(hs_instance* h, int kind, int phase, int B, const int16_t* groups, hs_pcg64* rng, int16_t* out,
                    int32_t* changed) {
-    return refine_common(h, kind, 1, 1, phase, B, groups, rng, out, nullptr, nullptr, changed);
+    // one pass never prices, so any d_pp <= 32 works (config 5 gains-only stress)
+    if (!h) return fail(-2, "null handle");
+    if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
+    if (kind < 0 || kind > 1) return fail(-2, "kind must be 0 (ours) or 1 (kl)");
+    if (kind == 0 && h->k == 1 && h->m >= 2)
+        return fail(-4, "zero-size array to reduction operation maximum which has no identity");
+    if (h->k > 32 || h->m > 64) return fail(-3, "passes support d_pp <= 32, d_dp <= 64");
+    DeviceGuard dg(h->device);
+    const int km = h->k * h->m;
+    DevBuf<int16_t> gi, go;
+    DevBuf<hs_pcg64> r;
+    DevBuf<int> ch;
+    DevBuf<double> mean;
+    DevBuf<uint32_t> mver;
+    CK(gi.alloc((size_t)B * km), "cudaMalloc");
+    CK(go.alloc((size_t)B * km), "cudaMalloc");
+    CK(r.alloc(B), "cudaMalloc");
+    CK(ch.alloc(B), "cudaMalloc");
+    CK(mean.alloc((size_t)B * h->n * h->k), "cudaMalloc");
+    CK(mver.alloc((size_t)B * h->n * h->k), "cudaMalloc");
+    CK(cudaMemcpy(gi.p, groups, (size_t)B * km * 2, cudaMemcpyHostToDevice), "H2D");
+    CK(cudaMemcpy(r.p, rng, sizeof(hs_pcg64) * B, cudaMemcpyHostToDevice), "H2D");
+    hs::PassArgs a{};
+    a.n = h->n;
+    a.k = h->k;
+    a.m = h->m;
+    a.kind = kind;
+    a.phase = phase;
+    a.sw = h->sw;
+    a.groups = gi.p;
+    a.rng = r.p;
+    a.out_groups = go.p;
+    a.changed = ch.p;
+    a.mean = mean.p;
+    a.mver = mver.p;
+    if (hs::launch_pass(a, B, 0)) return fail(-1, "pass launch", cudaGetLastError());
+    CK(cudaDeviceSynchronize(), "pass");
+    CK(cudaMemcpy(out, go.p, (size_t)B * km * 2, cudaMemcpyDeviceToHost), "D2H");
+    CK(cudaMemcpy(rng, r.p, sizeof(hs_pcg64) * B, cudaMemcpyDeviceToHost), "D2H");
+    if (changed) CK(cudaMemcpy(changed, ch.p, (size_t)B * 4, cudaMemcpyDeviceToHost), "D2H");
+    return 0;
 }
 
 int hs_crossover(int n, int d_pp, int d_dp, int device, int B, const int16_t* p1, const int16_t* p2, hs_pcg64* rng,

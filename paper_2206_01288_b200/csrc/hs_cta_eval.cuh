@@ -187,4 +187,81 @@ __device__ inline void cta_price(int n, int k, int m_rt, const double* DP, const
     datap = dp;
 }
 
+
+// ---------------------------------------------------------------------------
+// open_loop_tsp(heuristic=True) for k > 16 (combinatorics.py:299-342): nearest
+// neighbour from every start (ties to the smaller vertex), first-improvement
+// 2-opt with free path ends, cheapest float total wins, orientation
+// canonicalised.  One thread; O(k^4) like the reference.
+__device__ inline double path_cost_k(const double* E, int es, const int8_t* o, int k) {
+    double t = 0.0;
+    for (int i = k - 2; i >= 0; i--) t = E[o[i] * es + o[i + 1]] + t;
+    return t;
+}
+
+__device__ inline void two_opt_k(const double* E, int es, int8_t* o, int k) {
+    bool improved = true;
+    while (improved) {
+        improved = false;
+        for (int i = 0; i < k - 1; i++) {
+            for (int j = i + 1; j < k; j++) {
+                double before = 0.0, after = 0.0;
+                if (i > 0) {
+                    before += E[o[i - 1] * es + o[i]];
+                    after += E[o[i - 1] * es + o[j]];
+                }
+                if (j < k - 1) {
+                    before += E[o[j] * es + o[j + 1]];
+                    after += E[o[i] * es + o[j + 1]];
+                }
+                if (after < before) {
+                    for (int x = i, y = j; x < y; x++, y--) {
+                        int8_t t = o[x];
+                        o[x] = o[y];
+                        o[y] = t;
+                    }
+                    improved = true;
+                }
+            }
+        }
+    }
+}
+
+__device__ inline double nn_two_opt(const double* E, int es, int k, int8_t* best, int8_t* o) {
+    double best_total = kInf;
+    for (int start = 0; start < k; start++) {
+        uint64_t left = (k == 64 ? ~0ull : ((1ull << k) - 1)) & ~(1ull << start);
+        o[0] = (int8_t)start;
+        for (int t = 1; t < k; t++) {
+            int cur = o[t - 1], nxt = -1;
+            double bv = 0.0;
+            uint64_t l = left;
+            while (l) {
+                int v = __ffsll((long long)l) - 1;
+                l &= l - 1;
+                double x = E[cur * es + v];
+                if (nxt < 0 || x < bv) {  // min by (w, v)
+                    bv = x;
+                    nxt = v;
+                }
+            }
+            o[t] = (int8_t)nxt;
+            left &= ~(1ull << nxt);
+        }
+        two_opt_k(E, es, o, k);
+        double tot = path_cost_k(E, es, o, k);
+        if (tot < best_total) {
+            best_total = tot;
+            for (int i = 0; i < k; i++) best[i] = o[i];
+        }
+    }
+    if (best[0] > best[k - 1])
+        for (int x = 0, y = k - 1; x < y; x++, y--) {
+            int8_t t = best[x];
+            best[x] = best[y];
+            best[y] = t;
+        }
+    return path_cost_k(E, es, best, k);
+}
+
 }  // namespace hs

@@ -45,6 +45,7 @@ struct hs_instance {
     hs::HKBig hkb{};               // d_pp > 8: CTA evaluator schedule
     double* big_scratch[2] = {nullptr, nullptr};  // per-CTA Held-Karp slices (two stream sets)
     int big_blocks = 0;
+    double* heur_E = nullptr;      // d_pp > 16: per-CTA stage graphs for the heuristic path
     int* invalid = nullptr;
     hs::EvalPlan plan{};
     // host-buffer path

@@ -214,7 +214,7 @@ __device__ long long* g_prof = nullptr;
 // _fast_edge (:237-249): lexicographically first minimum intra-group pair,
 // lanes over (i, l) pairs, cached per group until the group changes.
 __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
-    if (s.valid[2] >> j & 1) {
+    if ((unsigned)s.valid[2] >> j & 1u) {
         a = s.fe[2 * j];
         b = s.fe[2 * j + 1];
         return;
@@ -254,7 +254,7 @@ __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
     if (lane == 0) {
         s.fe[2 * j] = (int16_t)a;
         s.fe[2 * j + 1] = (int16_t)b;
-        s.valid[2] |= 1 << j;
+        s.valid[2] |= (int)(1u << j);
         if (g_prof) {
             g_prof[9] += clock64() - f0;
             g_prof[10] += 1;
@@ -315,8 +315,8 @@ __device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa,
 }
 
 __device__ __forceinline__ void invalidate(LS& s, int j) {
-    s.valid[1] &= ~(1 << j);
-    s.valid[2] &= ~(1 << j);
+    s.valid[1] &= (int)~(1u << j);
+    s.valid[2] &= (int)~(1u << j);
     s.cver[j]++;
 }
 
@@ -362,10 +362,11 @@ __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
 // _home_costs (:287-291) for every group whose members changed
 __device__ inline void ensure_caches(LS& s, int lane) {
     const int k = s.k, n = s.n;
-    const int hv = s.valid[1];
-    if (hv == (1 << k) - 1) return;
+    const unsigned all = k >= 32 ? 0xffffffffu : (1u << k) - 1u;
+    const unsigned hv = (unsigned)s.valid[1];
+    if (hv == all) return;
     for (int i = 0; i < k; i++) {
-        if (hv >> i & 1) continue;
+        if (hv >> i & 1u) continue;
         const int16_t* g = s.G + i * s.cap;
         const int c = s.sz[i];
         for (int a = lane; a < c; a += kWarp) {
@@ -377,7 +378,7 @@ __device__ inline void ensure_caches(LS& s, int lane) {
         }
     }
     __syncwarp();
-    if (lane == 0) s.valid[1] = (1 << k) - 1;
+    if (lane == 0) s.valid[1] = (int)all;
     __syncwarp();
 }
 
@@ -1279,6 +1280,71 @@ __global__ void gains_kernel(int n, int k, int m, const double* __restrict__ sw,
         double t4 = psum(d2, gj2, m, d2);
         out[b] = t1 - t2 + t3 - t4 - 2.0 * sw[(size_t)d * n + d2];
     }
+}
+
+// ---------------------------------------------------------------------------
+// one refinement pass without pricing (gains-only stress, BASELINE config 5:
+// 1024 devices in 32 x 32 groups, where exact pricing is out of range).  One
+// warp per partition; the n x k mean cache lives in global memory.
+__global__ void __launch_bounds__(32) pass_kernel(PassArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x, b = blockIdx.x;
+    const int n = a.n, k = a.k, m = a.m, km = k * m, cap = m + 1;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        unsigned char* p = smem + off;
+        off += (bytes + 15) & ~(size_t)15;
+        return p;
+    };
+    LS s;
+    s.n = n;
+    s.k = k;
+    s.m = m;
+    s.cap = cap;
+    s.W = a.sw;
+    s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
+    s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
+    s.mean = a.mean + (size_t)b * n * k;
+    s.mver = a.mver + (size_t)b * n * k;
+    s.cver = reinterpret_cast<uint32_t*>(take((size_t)k * 4));
+    s.home = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.valid = reinterpret_cast<int*>(take(16));
+    s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+    s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
+    s.nlocked = reinterpret_cast<int*>(take(4));
+    s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
+    s.f64 = reinterpret_cast<double*>(take((size_t)(4 * cap + 2 * k + 2) * 8));
+    s.i32 = reinterpret_cast<int*>(take((size_t)(3 * k + 8) * 4));
+    s.grp_of = reinterpret_cast<int8_t*>(take((size_t)n));
+    for (int t = lane; t < n * k; t += kWarp) s.mver[t] = 0;
+    for (int t = lane; t < k; t += kWarp) s.cver[t] = 1;
+    __syncwarp();
+    Pcg64 rng;
+    rng.load(a.rng[b]);
+    load_groups(s, a.groups + (size_t)b * km, lane);
+    bool ch = a.kind == 0 ? ((s.sz[0] < 2) ? false : (a.phase % 2 == 0 ? pass_sweep(s, rng, lane) : pass_chains(s, lane)))
+                          : pass_kl(s, lane);
+    store_groups(s, a.out_groups + (size_t)b * km, lane);
+    if (lane == 0) {
+        a.changed[b] = ch;
+        rng.store(a.rng[b]);
+    }
+}
+
+size_t pass_smem_bytes(int n, int k, int m) {
+    auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
+    int cap = m + 1;
+    return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)k * 4) + al((size_t)n * 8) + al(16) +
+           al((size_t)k * 4) + al((size_t)((n + 31) >> 5) * 4) + al(4) + al((size_t)(k * k + cap) * 2) +
+           al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
+}
+
+int launch_pass(const PassArgs& a, int B, cudaStream_t st) {
+    if (B == 0) return 0;
+    size_t smem = pass_smem_bytes(a.n, a.k, a.m);
+    cudaFuncSetAttribute(pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pass_kernel<<<B, 32, smem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 // ---------------------------------------------------------------------------

@@ -62,6 +62,18 @@ struct RefineArgs {
     int* changed;           // [B] (single_pass)
 };
 
+// one pass, no pricing (any d_pp <= 32)
+struct PassArgs {
+    int n, k, m, kind, phase;
+    const double* sw;
+    const int16_t* groups;  // [B][k*m]
+    hs_pcg64* rng;          // [B]
+    int16_t* out_groups;
+    int* changed;
+    double* mean;     // [B][n*k] global scratch
+    uint32_t* mver;   // [B][n*k]
+};
+
 struct SearchShape {
     int n, k, m, max_passes, nvals;
     bool key16;
@@ -86,6 +98,7 @@ int launch_export(int islands, int P, int km, int E, const int16_t* pop, const d
                   double* out_cost, cudaStream_t st);
 int launch_import(int islands, int P, int km, int E, int16_t* pop, double* cost, int16_t* best, GAState* state,
                   const int16_t* mig, const double* mig_cost, const int32_t* src, cudaStream_t st);
+int launch_pass(const PassArgs& a, int B, cudaStream_t st);
 int launch_random_partitions(int n, int k, int m, int B, hs_pcg64* rng, int16_t* out, cudaStream_t st);
 
 }  // namespace hs

@@ -323,6 +323,33 @@ def gen_assignments():
     return out
 
 
+def gen_big():
+    """BASELINE config 5 (1024 devices): heuristic pricing at 32 x 32 and one
+    pass of each local-search flavour (the gains-only stress)."""
+    out = {"heuristic_costs": [], "passes": []}
+    g = make_random_graph(np.random.default_rng(0), 1024)
+    w = H.WorkloadSpec(32, 32, 268_435_456, 201_326_592)
+    rng = np.random.Generator(np.random.PCG64(77))
+    sw = S.SurrogateWeights.from_instance(g, w)
+    for t in range(2):
+        p = S.random_partition(rng, 1024, 32, 32)
+        cb = H.comm_cost(g, p, w, heuristic=True)
+        out["heuristic_costs"].append({"groups": groups_of(p), "total": hx(cb.total), "datap": hx(cb.datap),
+                                       "pipelinep": hx(cb.pipelinep), "order": list(cb.pipeline_order.order)})
+        for kind, phase in (("ours", 0), ("ours", 1), ("kl", 0)):
+            grs = [list(x) for x in p.groups]
+            prng = np.random.Generator(np.random.PCG64(500 + t))
+            t0 = time.perf_counter()
+            ch = S._pass_ours(sw.w, grs, prng, phase=phase) if kind == "ours" else S._pass_kl(sw.w, grs)
+            dt = time.perf_counter() - t0
+            st = prng.bit_generator.state
+            out["passes"].append({"kind": kind, "phase": phase, "seed": 500 + t, "groups": groups_of(p),
+                                  "changed": bool(ch), "out": grs, "seconds": dt,
+                                  "rng_after": [str(st["state"]["state"]), st["has_uint32"], st["uinteger"]]})
+        print("big", t, flush=True)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true", help="also run the 1000-generation GA anchors")
@@ -340,6 +367,8 @@ def main():
         (OUT / "search.json").write_text(json.dumps(gen_search()))
     if not only or "assign" in only:
         (OUT / "assignments.json").write_text(json.dumps(gen_assignments()))
+    if only and "big" in only:
+        (OUT / "big.json").write_text(json.dumps(gen_big()))
     if not only or "evolve" in only:
         jobs = list(EVOLVE_FAST)
         with ProcessPoolExecutor(max_workers=os.cpu_count()) as ex:

@@ -209,3 +209,23 @@ def test_oracle_assignments():
 def test_oracle_evolve_1000_generations(idx):
     """The GA time-to-converge anchors (pop 64, 1000 gens, ours, seed 0)."""
     _check_run(I.fixture("evolve_1000.json")["runs"][idx])
+
+
+def test_oracle_config5_heuristic_and_passes():
+    """Config 5 (1024 devices, 32 x 32): heuristic pricing and one pass of each
+    flavour, as the reference computed them (tests/golden/big.json)."""
+    from paper_2206_01288_b200.netmodel import random_graph
+    from paper_2206_01288_b200.workload import WorkloadSpec
+    g = random_graph(0, 1024)
+    w = WorkloadSpec(32, 32, 268_435_456, 201_326_592)
+    orc = O.Oracle.of(g, w)
+    big = I.fixture("big.json")
+    for c in big["heuristic_costs"]:
+        t, d, p, order = orc.comm_cost_heuristic(np.array(c["groups"], dtype=np.int32))
+        assert t == fx(c["total"]) and d == fx(c["datap"]) and p == fx(c["pipelinep"])
+        assert list(order) == c["order"]
+    for c in big["passes"]:
+        st = O.rng_state(c["seed"])
+        ch, out = orc.one_pass(np.array(c["groups"], dtype=np.int32), c["kind"], st, c["phase"])
+        assert ch == c["changed"] and out.tolist() == c["out"]
+        assert _rng_after(st) == c["rng_after"]
