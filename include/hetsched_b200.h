@@ -147,6 +147,16 @@ int hs_gains(int n, int d_pp, int d_dp, int device, const double *sw, int kind, 
  * members ascending) */
 int hs_random_partitions(int n, int d_pp, int d_dp, int device, int B, hs_pcg64 *rng, int16_t *out);
 
+/* ---------------- exhaustive search (costmodel.py:232-266) ------------------ */
+
+/* number of balanced partitions of n devices into groups of d_dp (-1 if
+ * d_dp does not divide n) */
+int64_t hs_count_partitions(int n, int d_dp);
+/* partitions [start, start+count) of the reference's enumeration order
+ * (_balanced_partitions: lexicographic canonical keys) as int16
+ * [count][d_pp][d_dp] into device memory; n <= 64 */
+int hs_unrank_partitions(int n, int d_pp, int d_dp, int64_t start, int64_t count, int16_t *out, void *stream);
+
 /* ---------------- fixed layouts (evaluation.py) ---------------------------- */
 
 /* materialize (evaluation.py:162-192): grid int16 [B][d_dp][d_pp] (row i =

@@ -118,9 +118,12 @@ def lib():
         L.hs_materialize.argtypes = [vp, i64, vp, vp, vp]
         L.hs_evaluate_assignments.argtypes = [vp, i64, vp, vp, vp]
         L.hs_random_assignments.argtypes = [i32, i32, i32, i32, i32, pcg, vp, vp]
+        L.hs_count_partitions.argtypes = [i32, i32]
+        L.hs_unrank_partitions.argtypes = [i32, i32, i32, i64, i64, vp, vp]
         for name in EXPORTS:
             if name not in ("hs_version", "hs_last_error"):
                 getattr(L, name).restype = i32
+        L.hs_count_partitions.restype = i64
         _lib = L
         return L
 
@@ -129,7 +132,7 @@ EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_des
            "hs_eval_batch", "hs_eval_batch_ex", "hs_eval_batch_host", "hs_path_heuristic_batch", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
            "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
-           "hs_random_assignments")
+           "hs_random_assignments", "hs_count_partitions", "hs_unrank_partitions")
 
 
 def check(rc: int, what: str) -> None:

@@ -211,3 +211,41 @@ def pipeline_cost(cg, heuristic: bool = False) -> tuple[float, PathResult]:
     """Cheapest open chain through a coarsened edge matrix (costmodel.py:211-214)."""
     res = open_loop_tsp(cg.edge_cost if hasattr(cg, "edge_cost") else cg, heuristic=heuristic)
     return res.total, res
+
+
+MAX_BRUTE_FORCE_DEVICES = 8
+
+
+def brute_force_best(g, w, max_devices: int = MAX_BRUTE_FORCE_DEVICES, chunk: int = 1 << 20):
+    """Exhaustive optimum over all balanced partitions (costmodel.py:246-266).
+
+    Candidates are unranked on the GPU in the reference's enumeration order
+    (lexicographic canonical keys) and priced in bulk; ties keep the first,
+    i.e. the lexicographically smallest key.  ``max_devices`` defaults to the
+    reference's limit of 8; raise it (e.g. 16) for ground-truth optima the
+    reference cannot afford."""
+    validate_workload(w, g.lat.shape[0])
+    n = g.lat.shape[0]
+    if n > max_devices:
+        raise CostModelError(f"exhaustive search is limited to {max_devices} devices, got {n}")
+    if w.d_pp > 16:
+        raise CostModelError("exhaustive search needs exact pricing (d_pp <= 16)")
+    torch = N.torch_cuda()
+    inst = N.instance_for(g, w)
+    dev = f"cuda:{inst.device}"
+    total = int(N.lib().hs_count_partitions(n, w.d_dp))
+    best_t, best_i = None, -1
+    for start in range(0, total, chunk):
+        cnt = min(chunk, total - start)
+        parts = torch.empty((cnt, w.d_pp, w.d_dp), dtype=torch.int16, device=dev)
+        N.check(N.lib().hs_unrank_partitions(n, w.d_pp, w.d_dp, start, cnt, parts.data_ptr(),
+                                             N.stream_ptr(inst.device)), "hs_unrank_partitions")
+        tot = comm_cost_batch(g, parts, w)["total"].cpu().numpy()
+        i = int(np.argmin(tot))  # first minimum
+        if best_t is None or tot[i] < best_t:
+            best_t, best_i = tot[i], start + i
+    one = torch.empty((1, w.d_pp, w.d_dp), dtype=torch.int16, device=dev)
+    N.check(N.lib().hs_unrank_partitions(n, w.d_pp, w.d_dp, best_i, 1, one.data_ptr(), N.stream_ptr(inst.device)),
+            "hs_unrank_partitions")
+    p = Partition.from_groups(one.cpu().numpy()[0].tolist())
+    return p, comm_cost(g, p, w)
