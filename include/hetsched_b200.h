@@ -173,6 +173,30 @@ int hs_evaluate_assignments(hs_instance *h, int64_t B, const int16_t *grids, dou
  * grids int16 [B][d_dp][d_pp], orders int8 [B][d_pp]; host buffers. */
 int hs_random_assignments(int n, int d_pp, int d_dp, int device, int B, hs_pcg64 *rng, int16_t *grids, int8_t *orders);
 
+/* ---------------- single-matrix solvers behind coarsen() ------------------- */
+
+/* bottleneck_perfect_matching (combinatorics.py:134-144) of B matrices
+ * [B][m][m], m <= 64, entries finite and >= 0: value [B] (an exact entry)
+ * and the lexicographically smallest optimal pairing pairs [B][m] (row ->
+ * column; nullable).  Device pointers; replaces the per-pair Python loop
+ * in coarsen (costmodel.py:186-197). */
+int hs_bottleneck_match_batch(const double *w, int m, int64_t B, double *value, int8_t *pairs, int device,
+                              void *stream);
+/* datap_cost_group (costmodel.py:154-168) of G groups from gathered raw
+ * blocks lat/bw [G][m][m] (rows and columns = sorted members), m <= 128:
+ * out [G] = max row of numpy-pairwise sums of 2.0*(lat + dp_num/(ddp*bw))
+ * with a 0.0 diagonal.  ddp = (double)d_dp, dp_num = 8.0*c_dp (host
+ * formed).  Device pointers. */
+int hs_datap_group_batch(const double *lat, const double *bw, int m, int64_t G, double ddp, double dp_num, double *out,
+                         int device, void *stream);
+/* The reference's exhaustive oracles over all k! permutations, k <= 10, of
+ * one k x k matrix (device pointers): kind 0 = brute_force_bottleneck_
+ * matching (combinatorics.py:192-207, value = largest selected entry), kind
+ * 1 = brute_force_open_loop_tsp (:345-361, value = right-to-left path
+ * cost).  perm [k] = the first permutation in itertools order attaining the
+ * minimum, as the reference's strict `<` scan keeps. */
+int hs_brute_force(const double *w, int k, int kind, double *value, int8_t *perm, int device, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,18 +33,34 @@ class NativeError(RuntimeError):
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every .cu under csrc/ into lib/libhetsched_sm100a.so (sm_100a)."""
+    """Compile every .cu under csrc/ (in parallel, one object each) and link
+    lib/libhetsched_sm100a.so for sm_100a."""
     newest = max(p.stat().st_mtime for p in SOURCES)
     if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
         return LIB_PATH
-    LIB_PATH.parent.mkdir(exist_ok=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = LIB_PATH.parent / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    cus = [str(p) for p in sorted((PKG / "csrc").glob("*.cu"))]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    cus = sorted((PKG / "csrc").glob("*.cu"))
+
+    def one(cu: Path):
+        obj = objdir / (cu.stem + ".o")
+        r = subprocess.run([nvcc, *compile_flags, "-c", "-o", str(obj), str(cu)], capture_output=not verbose,
+                           text=True)
+        return obj, r
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cus), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(one, cus))
+    errs = [r.stderr for _, r in results if r.returncode]
+    if errs:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", str(tmp), *cus]
-    r = subprocess.run(cmd, capture_output=not verbose, text=True)
+    r = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+                        *[str(o) for o, _ in results]], capture_output=not verbose, text=True)
     if r.returncode:
-        raise RuntimeError(f"nvcc failed:\n{r.stderr}")
+        raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
@@ -119,6 +135,9 @@ def lib():
         L.hs_evaluate_assignments.argtypes = [vp, i64, vp, vp, vp]
         L.hs_random_assignments.argtypes = [i32, i32, i32, i32, i32, pcg, vp, vp]
         L.hs_count_partitions.argtypes = [i32, i32]
+        L.hs_bottleneck_match_batch.argtypes = [vp, i32, i64, vp, vp, i32, vp]
+        L.hs_datap_group_batch.argtypes = [vp, vp, i32, i64, dbl, dbl, vp, i32, vp]
+        L.hs_brute_force.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.hs_unrank_partitions.argtypes = [i32, i32, i32, i64, i64, vp, vp]
         for name in EXPORTS:
             if name not in ("hs_version", "hs_last_error"):
@@ -129,10 +148,12 @@ def lib():
 
 
 EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_destroy", "hs_instance_tables",
-           "hs_eval_batch", "hs_eval_batch_ex", "hs_eval_batch_host", "hs_path_heuristic_batch", "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
+           "hs_eval_batch", "hs_eval_batch_ex", "hs_eval_batch_host", "hs_path_heuristic_batch",
+           "hs_bottleneck_batch", "hs_path_batch", "hs_ga_create", "hs_ga_create_ex", "hs_ga_run",
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
            "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
-           "hs_random_assignments", "hs_count_partitions", "hs_unrank_partitions")
+           "hs_random_assignments", "hs_count_partitions", "hs_unrank_partitions", "hs_bottleneck_match_batch",
+           "hs_datap_group_batch", "hs_brute_force")
 
 
 def check(rc: int, what: str) -> None:

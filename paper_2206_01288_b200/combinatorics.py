@@ -88,6 +88,75 @@ def bottleneck_value(costs) -> float:
     return float(bottleneck_values(w[None])[0])
 
 
+def bottleneck_matchings(stack) -> tuple[np.ndarray, np.ndarray]:
+    """Optimal bottleneck [B] and lexicographically smallest optimal pairing
+    [B, m] (row -> column) of each matrix in a [B, m, m] stack (GPU)."""
+    a = np.ascontiguousarray(stack, dtype=np.float64)
+    if a.ndim != 3 or a.shape[1] != a.shape[2] or a.shape[1] == 0:
+        raise ValueError(f"expected a [B, m, m] stack, got shape {a.shape}")
+    if not np.all(np.isfinite(a)) or np.any(a < 0):
+        raise ValueError("cost matrix must be finite and nonnegative")
+    if a.shape[1] > MAX_GPU_MATCH_M:
+        raise ValueError(f"GPU bottleneck search supports m <= {MAX_GPU_MATCH_M}, got {a.shape[1]}")
+    B, m = a.shape[0], a.shape[1]
+    if B == 0:
+        return np.empty(0), np.empty((0, m), dtype=np.int64)
+    torch = N.torch_cuda()
+    dev = N.current_device()
+    w = torch.from_numpy(a).to(f"cuda:{dev}")
+    val = torch.empty(B, dtype=torch.float64, device=f"cuda:{dev}")
+    pairs = torch.empty((B, m), dtype=torch.int8, device=f"cuda:{dev}")
+    N.check(N.lib().hs_bottleneck_match_batch(w.data_ptr(), m, B, val.data_ptr(), pairs.data_ptr(), dev,
+                                              N.stream_ptr(dev)), "hs_bottleneck_match_batch")
+    return val.cpu().numpy(), pairs.cpu().numpy().astype(np.int64)
+
+
+def bottleneck_perfect_matching(costs) -> MatchingResult:
+    """Perfect matching minimizing the largest selected entry; among the
+    optimal ones, the lexicographically smallest pairing
+    (combinatorics.py:134-189)."""
+    w = _checked_square(costs, "cost matrix")
+    val, pairs = bottleneck_matchings(w[None])
+    return MatchingResult(tuple(int(x) for x in pairs[0]), float(val[0]))
+
+
+MAX_BRUTE_FORCE = 10
+
+
+def _brute_force(w: np.ndarray, kind: int) -> tuple[tuple[int, ...], float]:
+    k = w.shape[0]
+    if k > MAX_BRUTE_FORCE:
+        raise ValueError(f"brute force is limited to k <= {MAX_BRUTE_FORCE}, got {k}")
+    torch = N.torch_cuda()
+    dev = N.current_device()
+    t = torch.from_numpy(np.ascontiguousarray(w)).to(f"cuda:{dev}")
+    val = torch.empty(1, dtype=torch.float64, device=f"cuda:{dev}")
+    perm = torch.empty(k, dtype=torch.int8, device=f"cuda:{dev}")
+    N.check(N.lib().hs_brute_force(t.data_ptr(), k, kind, val.data_ptr(), perm.data_ptr(), dev, N.stream_ptr(dev)),
+            "hs_brute_force")
+    return tuple(int(x) for x in perm.cpu().numpy()), float(val.item())
+
+
+def brute_force_bottleneck_matching(costs) -> MatchingResult:
+    """All k! pairings on the GPU; the first (itertools order) optimum
+    (combinatorics.py:192-207)."""
+    w = _checked_square(costs, "cost matrix")
+    perm, val = _brute_force(w, 0)
+    return MatchingResult(perm, val)
+
+
+def brute_force_open_loop_tsp(weights) -> PathResult:
+    """Every directed vertex sequence on the GPU; the first optimum
+    (combinatorics.py:345-361)."""
+    w = _checked_symmetric(weights)
+    if w.shape[0] > MAX_BRUTE_FORCE:
+        raise ValueError(f"brute force is limited to k <= {MAX_BRUTE_FORCE}, got {w.shape[0]}")
+    if w.shape[0] == 1:
+        return PathResult((0,), 0.0)
+    perm, val = _brute_force(w, 1)
+    return PathResult(perm, val)
+
+
 def open_loop_tsps(stack) -> tuple[np.ndarray, np.ndarray]:
     """Exact Held-Karp totals [B] and orders [B, k] of a [B, k, k] stack (GPU, k <= 8)."""
     a = np.ascontiguousarray(stack, dtype=np.float64)

@@ -21,7 +21,7 @@ from typing import Iterable
 import numpy as np
 
 from . import _native as N
-from .combinatorics import PathResult, open_loop_tsp
+from .combinatorics import MatchingResult, PathResult, bottleneck_matchings, open_loop_tsp
 from .workload import validate_workload
 
 
@@ -88,6 +88,21 @@ class CostBreakdown:
             "per_group_datap": list(self.per_group_datap),
             "pipeline_order": list(self.pipeline_order.order),
         }
+
+
+@dataclass(frozen=True)
+class CoarsenedGraph:
+    """One vertex per group; edge_cost[j, j2] is the bottleneck of the pair
+    matrix rows sorted(group j) x columns sorted(group j2), matchings[(j, j2)]
+    (j < j2) its lexicographically smallest optimal pairing
+    (costmodel.py:99-111)."""
+
+    edge_cost: np.ndarray
+    matchings: dict
+
+    @property
+    def k(self) -> int:
+        return self.edge_cost.shape[0]
 
 
 def _check_partition(p, g, w) -> None:
@@ -205,6 +220,62 @@ def datap_cost(g, p, w) -> tuple[float, tuple[float, ...]]:
     _check_partition(p, g, w)
     cb = comm_cost(g, p, w)
     return cb.datap, cb.per_group_datap
+
+
+def datap_cost_group(g, group: Iterable[int], w) -> float:
+    """Seconds the slowest member of one data-parallel group spends syncing
+    (costmodel.py:154-168), priced on the GPU from the raw lat/bw entries."""
+    devs = sorted(int(d) for d in group)
+    if len(set(devs)) != len(devs):
+        raise CostModelError(f"duplicate device in group {devs}")
+    if len(devs) != w.d_dp:
+        raise CostModelError(f"group size {len(devs)} does not match d_dp {w.d_dp}")
+    if devs and (devs[0] < 0 or devs[-1] >= g.lat.shape[0]):
+        raise CostModelError(f"device out of range in group {devs}")
+    if len(devs) == 1:
+        return 0.0
+    return float(datap_cost_groups(g, np.asarray([devs]), w)[0])
+
+
+def datap_cost_groups(g, groups, w) -> np.ndarray:
+    """datap_cost_group of each row of int [G, d_dp] (members ascending)."""
+    idx = np.asarray(groups, dtype=np.int64)
+    G, m = idx.shape
+    if m > 128:
+        raise CostModelError(f"GPU datap pricing supports groups of <= 128 devices, got {m}")
+    if G == 0:
+        return np.empty(0)
+    lat = np.ascontiguousarray(np.asarray(g.lat)[idx[:, :, None], idx[:, None, :]])
+    bw = np.ascontiguousarray(np.asarray(g.bw)[idx[:, :, None], idx[:, None, :]])
+    torch = N.torch_cuda()
+    dev = N.current_device()
+    tl = torch.from_numpy(lat).to(f"cuda:{dev}")
+    tb = torch.from_numpy(bw).to(f"cuda:{dev}")
+    out = torch.empty(G, dtype=torch.float64, device=f"cuda:{dev}")
+    dp_num = float(8.0 * w.c_dp)
+    N.check(N.lib().hs_datap_group_batch(tl.data_ptr(), tb.data_ptr(), m, G, float(w.d_dp), dp_num, out.data_ptr(),
+                                         dev, N.stream_ptr(dev)), "hs_datap_group_batch")
+    return out.cpu().numpy()
+
+
+def coarsen(g, p, w) -> CoarsenedGraph:
+    """Collapse each group to a vertex; edges carry the bottleneck matching
+    (costmodel.py:186-197).  The C(k,2) pair matrices are gathered from the
+    GPU-built PP table and solved in one batched launch."""
+    _check_partition(p, g, w)
+    k = len(p.groups)
+    pp = N.instance_for(g, w).tables()[1]
+    pairs = [(j, j2) for j in range(k) for j2 in range(j + 1, k)]
+    grp = [np.asarray(gr, dtype=np.int64) for gr in p.groups]
+    edge = np.zeros((k, k))
+    matchings: dict = {}
+    if pairs:
+        stack = np.stack([pp[np.ix_(grp[j], grp[j2])] for j, j2 in pairs])
+        vals, prs = bottleneck_matchings(stack)
+        for (j, j2), v, pr in zip(pairs, vals, prs):
+            edge[j, j2] = edge[j2, j] = v
+            matchings[(j, j2)] = MatchingResult(tuple(int(x) for x in pr), float(v))
+    return CoarsenedGraph(edge, matchings)
 
 
 def pipeline_cost(cg, heuristic: bool = False) -> tuple[float, PathResult]:

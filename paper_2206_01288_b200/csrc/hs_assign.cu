@@ -293,4 +293,61 @@ int launch_random_assign(int n, int k, int m, int B, hs_pcg64* rngs, int16_t* sc
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+// bottleneck_perfect_matching (combinatorics.py:134-144) of B matrices
+// [B][m][m]: optimal threshold, then the lexicographically smallest pairing
+// among the perfect matchings that stay within it.  One thread per matrix.
+__global__ void bottleneck_match_kernel(const double* __restrict__ w, int m, int64_t B, double* __restrict__ value,
+                                        int8_t* __restrict__ pairs) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < B; b += (int64_t)gridDim.x * blockDim.x) {
+        const double* W = w + b * m * m;
+        double L = bottleneck_threshold<double>(m, [&](int r, int c) { return W[r * m + c]; }, kInf);
+        uint64_t adj[kMaxM];
+        for (int r = 0; r < m; r++) {
+            uint64_t row = 0;
+            for (int c = 0; c < m; c++)
+                if (W[r * m + c] <= L) row |= 1ull << c;
+            adj[r] = row;
+        }
+        value[b] = L;
+        if (pairs) lex_pairing(m, adj, pairs + b * m);
+    }
+}
+
+// datap_cost_group (costmodel.py:154-168) of G gathered m x m blocks of raw
+// lat / bw: dp_pair_seconds with a zero diagonal, numpy-pairwise row sums,
+// largest row.  One warp per group, one lane per row.
+__global__ void datap_group_kernel(const double* __restrict__ lat, const double* __restrict__ bw, int m, int64_t G,
+                                   double ddp, double dp_num, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < G; g += W) {
+        const double* L = lat + g * m * m;
+        const double* Bw = bw + g * m * m;
+        double best = -kInf;
+        for (int r = lane; r < m; r += kWarp) {
+            double s = pairwise_sum(m, [&](int c) {
+                return c == r ? 0.0 : 2.0 * (L[r * m + c] + dp_num / (ddp * Bw[r * m + c]));
+            });
+            best = dmax(best, s);
+        }
+        for (int o = 16; o; o >>= 1) best = dmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) out[g] = m == 1 ? 0.0 : best;
+    }
+}
+
+int launch_bottleneck_match(const double* w, int m, int64_t B, double* value, int8_t* pairs, cudaStream_t s) {
+    if (B == 0) return 0;
+    int blocks = (int)std::min<int64_t>((B + 63) / 64, 148 * 16);
+    bottleneck_match_kernel<<<blocks, 64, 0, s>>>(w, m, B, value, pairs);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_datap_group(const double* lat, const double* bw, int m, int64_t G, double ddp, double dp_num, double* out,
+                       cudaStream_t s) {
+    if (G == 0) return 0;
+    int blocks = (int)std::min<int64_t>((G + 7) / 8, 148 * 8);
+    datap_group_kernel<<<blocks, 256, 0, s>>>(lat, bw, m, G, ddp, dp_num, out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 }  // namespace hs

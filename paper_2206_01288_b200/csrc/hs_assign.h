@@ -26,5 +26,8 @@ int launch_evaluate(int n, int k, int m, const double* dp, const double* pp, con
                     double* out3, double* per_col, int sm_count, cudaStream_t s);
 int launch_random_assign(int n, int k, int m, int B, hs_pcg64* rngs, int16_t* scratch, int16_t* grids, int8_t* orders,
                          cudaStream_t s);
+int launch_bottleneck_match(const double* w, int m, int64_t B, double* value, int8_t* pairs, cudaStream_t s);
+int launch_datap_group(const double* lat, const double* bw, int m, int64_t G, double ddp, double dp_num, double* out,
+                       cudaStream_t s);
 
 }  // namespace hs

@@ -93,4 +93,26 @@ int hs_random_assignments(int n, int d_pp, int d_dp, int device, int B, hs_pcg64
     return 0;
 }
 
+int hs_bottleneck_match_batch(const double* w, int m, int64_t B, double* value, int8_t* pairs, int device,
+                              void* stream) {
+    if (m < 1 || m > 64) return fail(-3, "bottleneck matching: m must be in 1..64");
+    if (B < 0) return fail(-2, "negative batch");
+    if (B && (!w || !value)) return fail(-2, "null argument");
+    DeviceGuard dg(device);
+    if (hs::launch_bottleneck_match(w, m, B, value, pairs, (cudaStream_t)stream))
+        return fail(-1, "bottleneck matching launch", cudaGetLastError());
+    return 0;
+}
+
+int hs_datap_group_batch(const double* lat, const double* bw, int m, int64_t G, double ddp, double dp_num, double* out,
+                         int device, void* stream) {
+    if (m < 1 || m > 128) return fail(-3, "datap group: m must be in 1..128");
+    if (G < 0) return fail(-2, "negative batch");
+    if (G && (!lat || !bw || !out)) return fail(-2, "null argument");
+    DeviceGuard dg(device);
+    if (hs::launch_datap_group(lat, bw, m, G, ddp, dp_num, out, (cudaStream_t)stream))
+        return fail(-1, "datap group launch", cudaGetLastError());
+    return 0;
+}
+
 }  // extern "C"

@@ -350,6 +350,39 @@ def gen_big():
     return out
 
 
+def gen_api():
+    """Public single-call surface behind coarsen / datap_cost_group and the
+    exhaustive oracles (costmodel.py:154-197, combinatorics.py:192-207,345-361)."""
+    out = {"brute_matching": [], "brute_tsp": [], "coarsen": [], "datap_group": []}
+    rng = np.random.default_rng(99)
+    for k in list(range(1, 9)) + [9, 10]:
+        for t in range(4 if k < 9 else 1):
+            w = rng.integers(0, 3, size=(k, k)).astype(float) if t % 2 == 0 else rng.uniform(0, 5, size=(k, k))
+            r = H.brute_force_bottleneck_matching(w)
+            out["brute_matching"].append({"k": k, "w": [hx(x) for x in w.ravel()], "pairs": list(r.pairs),
+                                          "value": hx(r.bottleneck)})
+            s_ = (w + w.T) / 2.0
+            np.fill_diagonal(s_, 0.0)
+            r2 = H.brute_force_open_loop_tsp(s_)
+            out["brute_tsp"].append({"k": k, "w": [hx(x) for x in s_.ravel()], "order": list(r2.order),
+                                     "total": hx(r2.total)})
+        print("brute", k, flush=True)
+    for name, seed in (("case5", 1), ("r12_3x4", 2), ("r16_4x4", 3), ("r36_6x6", 4), ("config1", 5)):
+        g, w = instance(INSTANCES[name])
+        prng = np.random.Generator(np.random.PCG64(seed))
+        for t in range(3):
+            p = S.random_partition(prng, g.n, w.d_pp, w.d_dp)
+            cg = H.coarsen(g, p, w)
+            out["coarsen"].append({
+                "instance": name, "groups": groups_of(p),
+                "edge": [hx(x) for x in cg.edge_cost.ravel()],
+                "matchings": [[j, j2, list(r.pairs), hx(r.bottleneck)] for (j, j2), r in sorted(cg.matchings.items())]})
+            for grp in p.groups:
+                out["datap_group"].append({"instance": name, "group": list(grp),
+                                           "value": hx(H.datap_cost_group(g, grp, w))})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slow", action="store_true", help="also run the 1000-generation GA anchors")
@@ -367,6 +400,8 @@ def main():
         (OUT / "search.json").write_text(json.dumps(gen_search()))
     if not only or "assign" in only:
         (OUT / "assignments.json").write_text(json.dumps(gen_assignments()))
+    if not only or "api" in only:
+        (OUT / "api.json").write_text(json.dumps(gen_api()))
     if only and "big" in only:
         (OUT / "big.json").write_text(json.dumps(gen_big()))
     if not only or "evolve" in only:
