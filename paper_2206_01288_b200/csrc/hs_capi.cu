@@ -33,9 +33,10 @@ int fail(int code, const char* what, cudaError_t e) {
 
 // Held-Karp schedule for k <= 8 (see hs_eval.cuh, warp_held_karp): compact
 // offsets off[s] (entries for |s| >= 2, s ascending), and per state (s, u)
-// the word off[r] | dst << 10 | u << 20 | r << 23 with r = s \ u, grouped by
-// layer |s|.
-void hk_schedule(int k, std::vector<uint32_t>& st, std::vector<uint16_t>& hoff, int lay[18]) {
+// with r = s \ u the pre-decoded 16-byte word (byte offsets of h[r][.] and
+// h[s][u], the byte offsets v*8 of r's members ascending, u*kES), grouped
+// by layer |s|.
+void hk_schedule(int k, std::vector<uint4>& st, std::vector<uint16_t>& hoff, int lay[18]) {
     st.clear();
     hoff.assign((size_t)1 << k, 0);
     int acc = 0;
@@ -56,14 +57,23 @@ void hk_schedule(int k, std::vector<uint32_t>& st, std::vector<uint16_t>& hoff, 
                 int s = r | (1 << u);
                 uint32_t dst = hoff[s] + __builtin_popcount(s & ((1 << u) - 1));
                 uint32_t offr = __builtin_popcount(r) >= 2 ? hoff[r] : 0;
-                st.push_back(offr | (dst << 10) | ((uint32_t)u << 20) | ((uint32_t)r << 23));
+                uint32_t vb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int nv = 0;
+                for (int v = 0; v < k; v++)
+                    if (r >> v & 1) vb[nv++] = (uint32_t)v * 8;
+                uint4 w;
+                w.x = offr * 8 | (dst * 8) << 16;
+                w.y = vb[0] | vb[1] << 8 | vb[2] << 16 | vb[3] << 24;
+                w.z = vb[4] | vb[5] << 8 | vb[6] << 16 | ((uint32_t)u * hs::kES) << 24;
+                w.w = (uint32_t)r | (uint32_t)u << 8;
+                st.push_back(w);
             }
         }
     }
 }
 
 struct DeviceHK {
-    uint32_t* st = nullptr;
+    uint4* st = nullptr;
     uint16_t* hoff = nullptr;
     hs::HKTables t{};
 };
@@ -77,12 +87,12 @@ int get_hk(int device, int k, hs::HKTables* out) {
     auto it = g_hk.find(key);
     if (it == g_hk.end()) {
         DeviceHK d;
-        std::vector<uint32_t> st;
+        std::vector<uint4> st;
         std::vector<uint16_t> hoff;
         hk_schedule(k, st, hoff, d.t.lay);
-        CK(cudaMalloc(&d.st, std::max<size_t>(4, st.size() * 4)), "cudaMalloc hk");
+        CK(cudaMalloc(&d.st, std::max<size_t>(16, st.size() * 16)), "cudaMalloc hk");
         CK(cudaMalloc(&d.hoff, hoff.size() * 2), "cudaMalloc hk");
-        if (!st.empty()) CK(cudaMemcpy(d.st, st.data(), st.size() * 4, cudaMemcpyHostToDevice), "upload hk");
+        if (!st.empty()) CK(cudaMemcpy(d.st, st.data(), st.size() * 16, cudaMemcpyHostToDevice), "upload hk");
         CK(cudaMemcpy(d.hoff, hoff.data(), hoff.size() * 2, cudaMemcpyHostToDevice), "upload hk");
         d.t.states = d.st;
         d.t.nstates = (int)st.size();

@@ -220,48 +220,62 @@ struct Match8 {
 //
 // Compact table: h[off[s] + rank(u in s)] for u in s, |s| >= 2 (layer 1 is
 // implicit 0.0).  Iterating v over the bits of r = s\u in ascending order
-// visits h[off[r] + i] at consecutive i, so the h address is base + const.
-// Each state word: off[r] (bits 0-9) | dst index (10-19) | u (20-22) | r (23-30).
+// visits h[off[r] + i] at consecutive i, so that address is base + const.
+// Each state is pre-decoded on the host into 16 bytes (hk_schedule):
+//   x = off[r]*8 | dst*8 << 16          (byte offsets into h)
+//   y = v0*8 | v1*8 << 8 | v2*8 << 16 | v3*8 << 24
+//   z = v4*8 | v5*8 << 8 | v6*8 << 16 | (u*kES) << 24
+//   w = r | u << 8                      (for debugging / tools)
+// so one relaxation is PRMT + IADD + 2 LDS + DADD + DSETP + 2 FSEL.
 // Layers p = |s| live in [lay[p], lay[p+1]).
 constexpr int kES = 9;  // padded E row stride (bank spread)
 
+template <int I>
+__device__ __forceinline__ uint32_t hk_vbyte(uint32_t y, uint32_t z) {
+    return I < 4 ? __byte_perm(y, 0u, 0x4440u + I) : __byte_perm(z, 0u, 0x4440u + (I - 4));
+}
+
 template <int NV>
-__device__ __forceinline__ double hk_relax(const double* __restrict__ Eu, const double* __restrict__ hr, uint32_t r) {
-    double best = kInf;
+__device__ __forceinline__ double hk_relax(const char* Eu, const char* hr, uint32_t y, uint32_t z) {
+    double best = *reinterpret_cast<const double*>(Eu + hk_vbyte<0>(y, z)) + *reinterpret_cast<const double*>(hr);
 #pragma unroll
-    for (int i = 0; i < NV; i++) {
-        int v = __ffs(r) - 1;
-        r &= r - 1;
-        double c = Eu[v] + hr[i];
+    for (int i = 1; i < NV; i++) {
+        uint32_t vb = i < 4 ? __byte_perm(y, 0u, 0x4440u + i) : __byte_perm(z, 0u, 0x4440u + (i - 4));
+        double c = *reinterpret_cast<const double*>(Eu + vb) + *reinterpret_cast<const double*>(hr + 8 * i);
         best = c < best ? c : best;
     }
     return best;
 }
 
-__device__ inline double warp_held_karp(int k, const double* E, double* h, const uint32_t* states, const int* lay,
+template <int NV>
+__device__ __forceinline__ void hk_layer(const char* Eb, char* hb, const uint4* states, int beg, int end, int lane) {
+    for (int idx = beg + lane; idx < end; idx += kWarp) {
+        const uint4 st = states[idx];
+        const char* Eu = Eb + (st.z >> 24) * 8;
+        double best;
+        if (NV == 1)  // w[u][v] + 0.0 == w[u][v]
+            best = *reinterpret_cast<const double*>(Eu + (st.y & 0xFFu));
+        else
+            best = hk_relax<NV>(Eu, hb + (st.x & 0xFFFFu), st.y, st.z);
+        *reinterpret_cast<double*>(hb + (st.x >> 16)) = best;
+    }
+}
+
+__device__ inline double warp_held_karp(int k, const double* E, double* h, const uint4* states, const int* lay,
                                         int lane) {
     if (k == 1) return 0.0;
+    const char* Eb = reinterpret_cast<const char*>(E);
+    char* hb = reinterpret_cast<char*>(h);
     for (int p = 2; p <= k; p++) {
-        const int end = lay[p + 1];
-        uint32_t wn = lay[p] + lane < end ? states[lay[p] + lane] : 0u;
-        for (int idx = lay[p] + lane; idx < end; idx += kWarp) {
-            uint32_t w = wn;
-            if (idx + kWarp < end) wn = states[idx + kWarp];  // prefetch the next state word
-            uint32_t r = w >> 23;
-            int u = (w >> 20) & 7;
-            const double* Eu = E + u * kES;
-            const double* hr = h + (w & 0x3FF);
-            double best;
-            switch (p) {
-                case 2: best = Eu[__ffs(r) - 1]; break;  // w[u][v] + 0.0 == w[u][v]
-                case 3: best = hk_relax<2>(Eu, hr, r); break;
-                case 4: best = hk_relax<3>(Eu, hr, r); break;
-                case 5: best = hk_relax<4>(Eu, hr, r); break;
-                case 6: best = hk_relax<5>(Eu, hr, r); break;
-                case 7: best = hk_relax<6>(Eu, hr, r); break;
-                default: best = hk_relax<7>(Eu, hr, r); break;
-            }
-            h[(w >> 10) & 0x3FF] = best;
+        const int beg = lay[p], end = lay[p + 1];
+        switch (p) {
+            case 2: hk_layer<1>(Eb, hb, states, beg, end, lane); break;
+            case 3: hk_layer<2>(Eb, hb, states, beg, end, lane); break;
+            case 4: hk_layer<3>(Eb, hb, states, beg, end, lane); break;
+            case 5: hk_layer<4>(Eb, hb, states, beg, end, lane); break;
+            case 6: hk_layer<5>(Eb, hb, states, beg, end, lane); break;
+            case 7: hk_layer<6>(Eb, hb, states, beg, end, lane); break;
+            default: hk_layer<7>(Eb, hb, states, beg, end, lane); break;
         }
         __syncwarp();
     }

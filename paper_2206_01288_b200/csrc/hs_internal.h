@@ -8,7 +8,7 @@ namespace hs {
 // Held-Karp schedule for one k (<= 8): packed state words grouped by layer
 // (see hs_eval.cuh), layer starts, and compact offsets off[s].
 struct HKTables {
-    const uint32_t* states;
+    const uint4* states;  // 16-byte pre-decoded states (hs_eval.cuh, warp_held_karp)
     int nstates;
     int lay[18];
     const uint16_t* hoff;

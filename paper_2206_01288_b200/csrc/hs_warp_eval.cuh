@@ -9,18 +9,18 @@ namespace hs {
 
 // Per-CTA copy of the Held-Karp state list and compact offsets.
 struct HKSmem {
-    const uint32_t* states;
+    const uint4* states;
     const int* lay;
     const uint16_t* hoff;
 };
 
 __host__ __device__ __forceinline__ size_t hk_smem_bytes(const HKTables& t) {
-    return (((size_t)t.nstates * 4 + 15) & ~(size_t)15) + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
+    return (size_t)t.nstates * 16 + 80 + (((size_t)t.nhoff * 2 + 15) & ~(size_t)15);
 }
 
 __device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* base) {
-    uint32_t* st = reinterpret_cast<uint32_t*>(base);
-    size_t off = ((size_t)t.nstates * 4 + 15) & ~(size_t)15;
+    uint4* st = reinterpret_cast<uint4*>(base);
+    size_t off = (size_t)t.nstates * 16;
     int* lay = reinterpret_cast<int*>(base + off);
     off += 80;
     uint16_t* hoff = reinterpret_cast<uint16_t*>(base + off);
