@@ -72,6 +72,49 @@ void hk_schedule(int k, std::vector<uint4>& st, std::vector<uint16_t>& hoff, int
     }
 }
 
+// Two-layer (ping-pong) variant: layer p's entries live in buffer p & 1 (each
+// buffer as large as the widest layer), so h needs 2 * max_p C(k,p)*p
+// doubles instead of k*2^(k-1) - k.  Same state words, offsets re-based; the
+// compact table (and so order reconstruction) is not kept.
+void hk_schedule_roll(int k, std::vector<uint4>& st, int lay[18], int* final_off, int* hsize) {
+    st.clear();
+    std::vector<uint32_t> loc((size_t)1 << k, 0), cnt(k + 1, 0);
+    for (int s = 0; s < (1 << k); s++) {
+        int p = __builtin_popcount(s);
+        loc[s] = cnt[p] * p;
+        cnt[p]++;
+    }
+    uint32_t S = 0;
+    for (int p = 2; p <= k; p++) S = std::max<uint32_t>(S, cnt[p] * p);
+    auto base = [&](int p) { return (p & 1) ? S : 0u; };
+    for (int i = 0; i < 18; i++) lay[i] = 0;
+    for (int p = 0; p < 18; p++) {
+        lay[p] = (int)st.size();
+        if (p < 2 || p > k) continue;
+        for (int r = 0; r < (1 << k); r++) {
+            if (__builtin_popcount(r) != p - 1) continue;
+            for (int u = 0; u < k; u++) {
+                if (r >> u & 1) continue;
+                int s = r | (1 << u);
+                uint32_t dst = base(p) + loc[s] + __builtin_popcount(s & ((1 << u) - 1));
+                uint32_t offr = p - 1 >= 2 ? base(p - 1) + loc[r] : 0;
+                uint32_t vb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                int nv = 0;
+                for (int v = 0; v < k; v++)
+                    if (r >> v & 1) vb[nv++] = (uint32_t)v * 8;
+                uint4 w;
+                w.x = offr * 8 | (dst * 8) << 16;
+                w.y = vb[0] | vb[1] << 8 | vb[2] << 16 | vb[3] << 24;
+                w.z = vb[4] | vb[5] << 8 | vb[6] << 16 | ((uint32_t)u * hs::kES) << 24;
+                w.w = (uint32_t)r | (uint32_t)u << 8;
+                st.push_back(w);
+            }
+        }
+    }
+    *final_off = (int)base(k);
+    *hsize = (int)(2 * S);
+}
+
 struct DeviceHK {
     uint4* st = nullptr;
     uint16_t* hoff = nullptr;
@@ -79,17 +122,20 @@ struct DeviceHK {
 };
 
 std::mutex g_hk_mu;
-std::map<std::pair<int, int>, DeviceHK> g_hk;  // (device, k)
+std::map<std::pair<int, int>, DeviceHK> g_hk;  // (device, k) compact; (device, -k) two-layer
 
-int get_hk(int device, int k, hs::HKTables* out) {
+int get_hk(int device, int k, hs::HKTables* out, bool roll) {
     std::lock_guard<std::mutex> lk(g_hk_mu);
-    auto key = std::make_pair(device, k);
+    auto key = std::make_pair(device, roll ? -k : k);
     auto it = g_hk.find(key);
     if (it == g_hk.end()) {
         DeviceHK d;
         std::vector<uint4> st;
         std::vector<uint16_t> hoff;
         hk_schedule(k, st, hoff, d.t.lay);
+        d.t.final_off = (k << (k - 1)) - 2 * k;
+        d.t.hsize = (k << (k - 1)) - k;
+        if (roll) hk_schedule_roll(k, st, d.t.lay, &d.t.final_off, &d.t.hsize);
         CK(cudaMalloc(&d.st, std::max<size_t>(16, st.size() * 16)), "cudaMalloc hk");
         CK(cudaMalloc(&d.hoff, hoff.size() * 2), "cudaMalloc hk");
         if (!st.empty()) CK(cudaMemcpy(d.st, st.data(), st.size() * 16, cudaMemcpyHostToDevice), "upload hk");
@@ -172,6 +218,7 @@ static hs::EvalArgs base_args(const hs_instance* h) {
     a.nvals = h->nvals;
     a.vals = h->vals;
     a.hk = h->hk;
+    a.hk_roll = h->hk_roll;
     return a;
 }
 
@@ -234,7 +281,8 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
         if (hs::launch_narrow((int64_t)nn, h->rank, h->rank16, 0)) return fail(-1, "narrow launch");
     }
     CK(cudaDeviceSynchronize(), "instance tables");
-    int rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk);
+    int rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk, false);
+    if (!rc) rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk_roll, true);
     if (rc) return rc;
     if (d_pp > 16) {
         // exact pricing is limited to 16 stages (combinatorics.py:243-249);

@@ -262,7 +262,7 @@ __device__ __forceinline__ void hk_layer(const char* Eb, char* hb, const uint4* 
 }
 
 __device__ inline double warp_held_karp(int k, const double* E, double* h, const uint4* states, const int* lay,
-                                        int lane) {
+                                        int lane, int final_off) {
     if (k == 1) return 0.0;
     const char* Eb = reinterpret_cast<const char*>(E);
     char* hb = reinterpret_cast<char*>(h);
@@ -279,8 +279,8 @@ __device__ inline double warp_held_karp(int k, const double* E, double* h, const
         }
         __syncwarp();
     }
-    // the full set's k entries are the last of the k*2^(k-1) - k slots
-    const double* hf = h + (k << (k - 1)) - 2 * k;
+    // the full set's k entries (compact table: the last k of k*2^(k-1) - k)
+    const double* hf = h + final_off;
     double tot = hf[0];
     for (int u = 1; u < k; u++) tot = dmin(tot, hf[u]);
     return tot;

@@ -10,7 +10,7 @@
 namespace hsx {
 
 int fail(int code, const char* what, cudaError_t e = cudaSuccess);
-int get_hk(int device, int k, hs::HKTables* out);
+int get_hk(int device, int k, hs::HKTables* out, bool roll = false);
 int get_hk_big(int device, int k, hs::HKBig* out);
 
 struct DeviceGuard {
@@ -42,6 +42,7 @@ struct hs_instance {
     uint16_t* rank16 = nullptr;
     int nvals = 0;
     hs::HKTables hk{};
+    hs::HKTables hk_roll{};        // two-layer schedule: batch pricing without stage order
     hs::HKBig hkb{};               // d_pp > 8: CTA evaluator schedule
     double* big_scratch[2] = {nullptr, nullptr};  // per-CTA Held-Karp slices (two stream sets)
     int big_blocks = 0;

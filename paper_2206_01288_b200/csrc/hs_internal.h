@@ -13,6 +13,8 @@ struct HKTables {
     int lay[18];
     const uint16_t* hoff;
     int nhoff;
+    int final_off;  // first of the full set's k entries in h
+    int hsize;      // doubles of h the schedule touches
 };
 
 // Held-Karp schedule for 9 <= k <= 16 (one CTA per candidate): 64-bit state
@@ -34,6 +36,7 @@ struct EvalArgs {
     int nvals;           // distinct PP values
     const double* vals;  // distinct PP values, ascending
     HKTables hk;
+    HKTables hk_roll;       // two-layer (ping-pong) schedule: no order reconstruction
     const int16_t* groups;  // [P][k][m], members ascending
     int64_t P;
     double* total;
@@ -48,6 +51,10 @@ struct EvalPlan {
     bool smem_tables, m8;
     int warps, blocks;
     size_t smem;
+    // no order output: two-layer Held-Karp schedule, smaller scratch, more warps
+    bool roll_smem_tables;
+    int roll_warps;
+    size_t roll_smem;
 };
 
 

@@ -48,13 +48,21 @@ __global__ void rank_kernel(int64_t nn, const double* __restrict__ pp, const dou
     }
 }
 
-template <bool kSmemTables, typename KeyT, bool kM8>
-__global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, ScratchLayout wl) {
+// warps per CTA of the batch evaluator (one CTA per SM; bounded by smem and
+// registers): with the compact Held-Karp table (stage order wanted) and with
+// the two-layer one (no order: 4.4 KB less scratch per warp)
+constexpr int kEvalWarps = 20;
+constexpr int kEvalWarpsRoll = 24;
+
+template <bool kSmemTables, typename KeyT, bool kM8, bool kRoll>
+__global__ void __launch_bounds__(32 * (kRoll ? kEvalWarpsRoll : kEvalWarps))
+    eval_warp_kernel(EvalArgs a, ScratchLayout wl) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int k = a.k, m = kM8 ? 8 : a.m, km = k * m;
-    HKSmem hk = hk_stage(a.hk, smem);
-    size_t off = hk_smem_bytes(a.hk);
+    const HKTables& hkt = kRoll ? a.hk_roll : a.hk;
+    HKSmem hk = hk_stage(hkt, smem);
+    size_t off = hk_smem_bytes(hkt);
     EvalView<KeyT> v = stage_tables<kSmemTables, KeyT>(a.n, k, m, a.dp, a.rank, a.vals, hk, smem, off);
     unsigned char* wbase = smem + off + (size_t)wid * wl.bytes;
     WarpScratch ws = scratch_at(wbase, wl);
@@ -82,7 +90,7 @@ __global__ void __launch_bounds__(512) eval_warp_kernel(EvalArgs a, ScratchLayou
             a.total[p] = datap + pipe;
             if (a.datap) a.datap[p] = datap;
             if (a.pipe) a.pipe[p] = pipe;
-            if (a.order) held_karp_order(k, ws.E, ws.h, hk.hoff, pipe, a.order + p * k);
+            if (!kRoll && a.order) held_karp_order(k, ws.E, ws.h, hk.hoff, pipe, a.order + p * k);
         }
         if (a.per_group && lane < k) a.per_group[p * k + lane] = ws.pg[lane];
         __syncwarp();
@@ -111,7 +119,7 @@ __global__ void path_batch_kernel(const double* __restrict__ w, int k, int64_t B
         const double* src = w + b * k * k;
         for (int i = lane; i < k * k; i += kWarp) E[(i / k) * kES + (i % k)] = src[i];
         __syncwarp();
-        double tt = warp_held_karp(k, E, h, hk.states, hk.lay, lane);
+        double tt = warp_held_karp(k, E, h, hk.states, hk.lay, lane, hk.final_off);
         if (lane == 0) {
             total[b] = tt;
             if (order) held_karp_order(k, E, h, hk.hoff, tt, order + b * k);
@@ -150,49 +158,69 @@ int launch_narrow(int64_t nn, const uint32_t* src, uint16_t* dst, cudaStream_t s
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan) {
-    ScratchLayout wl = scratch_layout(a.k, a.m);
-    size_t fixed = hk_bytes_host(a.hk);
+static int plan_for(const EvalArgs& a, const HKTables& t, int wmax, size_t smem_optin, bool* smem_tables, int* warps,
+                    size_t* smem) {
+    ScratchLayout wl = scratch_layout(a.k, a.m, t.hsize);
+    size_t fixed = hk_bytes_host(t);
     size_t keyb = a.key16 ? 2 : 4;
     size_t tables = (size_t)a.n * a.n * 8 + (((size_t)a.n * a.n * keyb + 15) & ~(size_t)15);
-    bool smem_tables = fixed + tables + 4 * (size_t)wl.bytes <= smem_optin;
-    size_t base = fixed + (smem_tables ? tables : 0);
+    *smem_tables = fixed + tables + 4 * (size_t)wl.bytes <= smem_optin;
+    size_t base = fixed + (*smem_tables ? tables : 0);
     if (base + wl.bytes > smem_optin) return -2;
-    int W = (int)std::min<size_t>(16, (smem_optin - base) / wl.bytes);
-    plan->smem_tables = smem_tables;
-    plan->warps = W;
-    plan->smem = base + (size_t)W * wl.bytes;
+    *warps = (int)std::min<size_t>(wmax, (smem_optin - base) / wl.bytes);
+    *smem = base + (size_t)*warps * wl.bytes;
+    return 0;
+}
+
+int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan) {
+    if (plan_for(a, a.hk, kEvalWarps, smem_optin, &plan->smem_tables, &plan->warps, &plan->smem)) return -2;
+    if (plan_for(a, a.hk_roll, kEvalWarpsRoll, smem_optin, &plan->roll_smem_tables, &plan->roll_warps,
+                 &plan->roll_smem))
+        return -2;
     plan->blocks = sm_count;
     plan->m8 = a.key16 && a.m == 8 && a.nvals <= 0x8000;
     return 0;
 }
 
-template <bool S, typename KT, bool M8>
-static void launch_one(const EvalArgs& a, const EvalPlan& plan, const ScratchLayout& wl, int blocks, cudaStream_t s) {
-    cudaFuncSetAttribute(eval_warp_kernel<S, KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem);
-    eval_warp_kernel<S, KT, M8><<<blocks, plan.warps * 32, plan.smem, s>>>(a, wl);
+template <bool S, typename KT, bool M8, bool R>
+static void launch_one(const EvalArgs& a, int warps, size_t smem, int blocks, cudaStream_t s) {
+    ScratchLayout wl = scratch_layout(a.k, a.m, R ? a.hk_roll.hsize : a.hk.hsize);
+    cudaFuncSetAttribute(eval_warp_kernel<S, KT, M8, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eval_warp_kernel<S, KT, M8, R><<<blocks, warps * 32, smem, s>>>(a, wl);
+}
+
+template <bool R>
+static void launch_variant(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s) {
+    const int warps = R ? plan.roll_warps : plan.warps;
+    const size_t smem = R ? plan.roll_smem : plan.smem;
+    const bool st = R ? plan.roll_smem_tables : plan.smem_tables;
+    int blocks = (int)std::min<int64_t>(plan.blocks, (a.P + warps - 1) / warps);
+    if (plan.m8) {
+        if (st)
+            launch_one<true, uint16_t, true, R>(a, warps, smem, blocks, s);
+        else
+            launch_one<false, uint16_t, true, R>(a, warps, smem, blocks, s);
+    } else if (a.key16) {
+        if (st)
+            launch_one<true, uint16_t, false, R>(a, warps, smem, blocks, s);
+        else
+            launch_one<false, uint16_t, false, R>(a, warps, smem, blocks, s);
+    } else {
+        if (st)
+            launch_one<true, uint32_t, false, R>(a, warps, smem, blocks, s);
+        else
+            launch_one<false, uint32_t, false, R>(a, warps, smem, blocks, s);
+    }
 }
 
 int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s) {
     if (a.P == 0) return 0;
-    ScratchLayout wl = scratch_layout(a.k, a.m);
-    int blocks = (int)std::min<int64_t>(plan.blocks, (a.P + plan.warps - 1) / plan.warps);
-    if (plan.m8) {
-        if (plan.smem_tables)
-            launch_one<true, uint16_t, true>(a, plan, wl, blocks, s);
-        else
-            launch_one<false, uint16_t, true>(a, plan, wl, blocks, s);
-    } else if (a.key16) {
-        if (plan.smem_tables)
-            launch_one<true, uint16_t, false>(a, plan, wl, blocks, s);
-        else
-            launch_one<false, uint16_t, false>(a, plan, wl, blocks, s);
-    } else {
-        if (plan.smem_tables)
-            launch_one<true, uint32_t, false>(a, plan, wl, blocks, s);
-        else
-            launch_one<false, uint32_t, false>(a, plan, wl, blocks, s);
-    }
+    // without an order output the compact table (needed to walk the optimal
+    // path back) is not kept: two-layer schedule, more warps per SM
+    if (a.order)
+        launch_variant<false>(a, plan, s);
+    else
+        launch_variant<true>(a, plan, s);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -12,6 +12,7 @@ struct HKSmem {
     const uint4* states;
     const int* lay;
     const uint16_t* hoff;
+    int final_off;
 };
 
 __host__ __device__ __forceinline__ size_t hk_smem_bytes(const HKTables& t) {
@@ -27,7 +28,7 @@ __device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* bas
     for (int i = threadIdx.x; i < t.nstates; i += blockDim.x) st[i] = t.states[i];
     for (int i = threadIdx.x; i < t.nhoff; i += blockDim.x) hoff[i] = t.hoff[i];
     if (threadIdx.x < 18) lay[threadIdx.x] = t.lay[threadIdx.x];
-    return HKSmem{st, lay, hoff};
+    return HKSmem{st, lay, hoff, t.final_off};
 }
 
 // What a warp reads to price a candidate (tables in smem or global).
@@ -53,10 +54,12 @@ struct ScratchLayout {
     int h_off, e_off, pg_off, mem_off, seen_off, bytes;
 };
 
-__host__ __device__ inline ScratchLayout scratch_layout(int k, int m) {
+// hsize: doubles of Held-Karp table (default: the compact table; the
+// two-layer schedule needs less, HKTables::hsize)
+__host__ __device__ inline ScratchLayout scratch_layout(int k, int m, int hsize = -1) {
     ScratchLayout wl;
     int km = k * m;
-    int hk = (k << (k - 1)) - k;
+    int hk = hsize >= 0 ? hsize : (k << (k - 1)) - k;
     int hsz = hk > km ? hk : km;
     int o = 0;
     wl.h_off = o;
@@ -165,7 +168,7 @@ __device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s,
     }
     if (lane < k) E[lane * kES + lane] = 0.0;
     __syncwarp();
-    pipe = warp_held_karp(k, E, h, v.hk.states, v.hk.lay, lane);
+    pipe = warp_held_karp(k, E, h, v.hk.states, v.hk.lay, lane, v.hk.final_off);
     double dp = s.pg[0];
     for (int g = 1; g < k; g++) dp = dmax(dp, s.pg[g]);
     datap = dp;

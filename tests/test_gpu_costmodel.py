@@ -193,3 +193,51 @@ def test_path_solver_k_9_to_16_vs_oracle():
         for i in range(len(stack)):
             o, t = O.open_loop_tsp(stack[i])
             assert tot[i] == t and tuple(order[i]) == o
+
+
+@pytest.mark.parametrize("name", sorted(_gpu_names()))
+def test_no_order_evaluator_matches_golden(name):
+    """order=False prices with the two-layer Held-Karp schedule (no compact
+    table kept, more warps per SM); same bits as the golden vectors."""
+    g, w = I.instance(name)
+    C = I.costs()
+    parts = C[f"{name}/parts"]
+    r = hs.comm_cost_batch(g, parts, w, per_group=True)
+    assert np.array_equal(r["total"], C[f"{name}/total"])
+    assert np.array_equal(r["datap"], C[f"{name}/datap"])
+    assert np.array_equal(r["pipelinep"], C[f"{name}/pipelinep"])
+    assert np.array_equal(r["per_group"], C[f"{name}/per_group"])
+
+
+def test_no_order_evaluator_invalid_ragged_and_offset_views():
+    import torch
+    g, w = I.instance("case5")
+    parts = _random_parts(21, 1000, 64, 8, 8)
+    ref = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())[0]
+    dev = torch.from_numpy(parts).cuda()
+    assert np.array_equal(hs.comm_cost_batch(g, dev, w)["total"].cpu().numpy(), ref)
+    assert np.array_equal(hs.comm_cost_batch(g, dev, w, order=True)["total"].cpu().numpy(), ref)
+    # a view at a 2-byte offset
+    buf = torch.empty(1000 * 64 + 1, dtype=torch.int16, device="cuda")
+    buf[1:] = dev.reshape(-1)
+    view = buf[1:].view(1000, 8, 8)
+    assert np.array_equal(hs.comm_cost_batch(g, view, w)["total"].cpu().numpy(), ref)
+    # malformed candidates scattered through the batch
+    bad = parts.copy()
+    for i in (0, 31, 32, 500, 999):
+        bad[i, 3, 2] = bad[i, 3, 1]
+    with pytest.raises(hs.CostModelError, match="5 of 1000"):
+        hs.comm_cost_batch(g, bad, w)
+    from paper_2206_01288_b200 import _native as N
+    inst = N.instance_for(g, w)
+    t = torch.from_numpy(bad).cuda()
+    tot = torch.empty(1000, dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().hs_eval_batch(inst.handle, t.data_ptr(), 1000, tot.data_ptr(), None, None, None, None,
+                                  cnt.data_ptr(), N.stream_ptr(inst.device)), "hs_eval_batch")
+    got = tot.cpu().numpy()
+    assert int(cnt.item()) == 5
+    good = np.ones(1000, bool)
+    good[[0, 31, 32, 500, 999]] = False
+    assert np.isnan(got[~good]).all()
+    assert np.array_equal(got[good], ref[good])
