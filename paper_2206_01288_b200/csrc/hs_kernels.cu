@@ -52,7 +52,7 @@ __global__ void rank_kernel(int64_t nn, const double* __restrict__ pp, const dou
 // registers): with the compact Held-Karp table (stage order wanted) and with
 // the two-layer one (no order: 4.4 KB less scratch per warp)
 constexpr int kEvalWarps = 20;
-constexpr int kEvalWarpsRoll = 24;
+constexpr int kEvalWarpsRoll = 28;
 
 template <bool kSmemTables, typename KeyT, bool kM8, bool kRoll>
 __global__ void __launch_bounds__(32 * (kRoll ? kEvalWarpsRoll : kEvalWarps))
