@@ -788,8 +788,8 @@ __device__ inline Pricer<KeyT, kM8, kCta> make_pricer(int n, int k, int m, const
     Pricer<KeyT, kM8, kCta> pr;
     HKSmem hk{};
     if constexpr (!kCta) {
-        hk = hk_stage(hkt, smem);
-        off = hk_smem_bytes(hkt);
+        hk = hk_global(hkt, smem);
+        off = kHKGlobalBytes;
     }
     pr.v = stage_tables<kSmemTables, KeyT>(n, k, m, dp, rank, vals, hk, smem, off);
     if constexpr (kCta) {
@@ -1364,7 +1364,7 @@ static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P, bo
     auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
     ScratchLayout wl = scratch_layout(sh.k <= 8 ? sh.k : 8, sh.m);
     int km = sh.k * sh.m, ms = 1 + sh.max_passes;
-    size_t b = sh.k <= 8 ? hk_smem_bytes(sh.hk) + (size_t)W * wl.bytes : al(cta_scratch_bytes(sh.k, sh.m));
+    size_t b = sh.k <= 8 ? kHKGlobalBytes + (size_t)W * wl.bytes : al(cta_scratch_bytes(sh.k, sh.m));
     if (smem_tables)
         b += (size_t)sh.n * sh.n * 8 + al((size_t)sh.n * sh.n * (sh.key16 ? 2 : 4)) + (size_t)sh.n * sh.n * 8;
     size_t isl = al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) +

@@ -31,6 +31,17 @@ __device__ __forceinline__ HKSmem hk_stage(const HKTables& t, unsigned char* bas
     return HKSmem{st, lay, hoff, t.final_off};
 }
 
+// Same schedule left in global memory (L1-resident after first use), only
+// the 18 layer bounds staged: for kernels whose shared memory is better spent
+// on other state (the GA), where pricing is a small share of the time.
+constexpr size_t kHKGlobalBytes = 80;
+
+__device__ __forceinline__ HKSmem hk_global(const HKTables& t, unsigned char* base) {
+    int* lay = reinterpret_cast<int*>(base);
+    if (threadIdx.x < 18) lay[threadIdx.x] = t.lay[threadIdx.x];
+    return HKSmem{t.states, lay, t.hoff, t.final_off};
+}
+
 // What a warp reads to price a candidate (tables in smem or global).
 template <typename KeyT>
 struct EvalView {
