@@ -26,7 +26,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # rank 0 prints exactly one JSON line
+# rank 0 prints exactly one JSON line on stdout: NCCL's own messages (its
+# version banner included) go to stderr
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "layout cost-evals/sec (N=64, D_PP=8xD_DP=8)"
 WORKLOAD = ("paper setting: 64 devices, D_PP=8 x D_DP=8, GPT3-XL tasklets "
