@@ -105,7 +105,19 @@ __device__ Key bottleneck_threshold(int m, const At& R, Key key_max) {
 // of row r; keys must be < 0x8000.  Adjacency at threshold L is one uint64
 // (bit 8r+c), built branch-free: per half, (0x8000|L) - key has bit 15 set
 // iff key <= L, and never borrows across halves.  Matching state lives in
-// packed 4-bit fields (0xF = free).
+// packed fields (row -> column nibbles, column -> row bit bytes), so a BFS
+// step takes all of a row's new columns at once without a per-column loop.
+// bit i of x (i < 8) -> nibble i = 0xF
+__device__ __forceinline__ uint32_t nibble_mask(uint32_t x) {
+    uint32_t t = (x & 0xFu) | ((x & 0xF0u) << 12);
+    t = (t | (t << 6)) & 0x03030303u;
+    t = (t | (t << 3)) & 0x11111111u;
+    return t * 0xFu;
+}
+
+// bit i of x (i < 4) -> byte i = 0xFF
+__device__ __forceinline__ uint32_t byte_mask4(uint32_t x) { return ((x * 0x00204081u) & 0x01010101u) * 0xFFu; }
+
 struct Match8 {
     __device__ __forceinline__ static uint32_t get4(uint32_t x, int i) { return (x >> (4 * i)) & 0xFu; }
     __device__ __forceinline__ static uint32_t set4(uint32_t x, int i, uint32_t v) {
@@ -146,15 +158,20 @@ struct Match8 {
         uint32_t c2 = __vmaxu2(__vmaxu2(cm0, cm1), __vmaxu2(cm2, cm3));
         L = max(L, max(c2 & 0xFFFFu, c2 >> 16));
         uint64_t adj = adjacency(K, L);
-        uint32_t mrow = 0xFFFFFFFFu, mcol = 0xFFFFFFFFu, used = 0, unmatched = 0;
+        // matching: mrow row -> column nibble (0xF free); mc byte c = bit of
+        // the row holding column c (0 if free); mcols = held columns
+        uint32_t mrow = 0xFFFFFFFFu, mc_lo = 0, mc_hi = 0, mcols = 0, unmatched = 0;
 #pragma unroll
         for (int r = 0; r < 8; r++) {
-            uint32_t av = (uint32_t)(adj >> (8 * r)) & 0xFFu & ~used;
+            uint32_t av = (uint32_t)(adj >> (8 * r)) & 0xFFu & ~mcols;
             if (av) {
                 uint32_t c = __ffs(av) - 1;
-                used |= 1u << c;
+                mcols |= 1u << c;
                 mrow = set4(mrow, r, c);
-                mcol = set4(mcol, c, r);
+                if (c < 4)
+                    mc_lo |= (1u << r) << (8 * c);
+                else
+                    mc_hi |= (1u << r) << (8 * (c - 4));
             } else {
                 unmatched |= 1u << r;
             }
@@ -165,23 +182,25 @@ struct Match8 {
             uint32_t rows_in = 1u << u, cols_in = 0, frontier = rows_in, parent = 0;
             int found = -1;
             for (;;) {
-                while (frontier && found < 0) {
-                    int r = __ffs(frontier) - 1;
+                // alternating BFS; a popped row takes all its new columns at
+                // once (bit-parallel), stopping at the lowest free one
+                while (frontier) {
+                    uint32_t r = __ffs(frontier) - 1;
                     frontier &= frontier - 1;
                     uint32_t cand = (uint32_t)(adj >> (8 * r)) & 0xFFu & ~cols_in;
-                    while (cand) {
-                        int c = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        parent = set4(parent, c, (uint32_t)r);
-                        cols_in |= 1u << c;
-                        uint32_t rr = get4(mcol, c);
-                        if (rr == 0xFu) {
-                            found = c;
-                            break;
-                        }
-                        rows_in |= 1u << rr;
-                        frontier |= 1u << rr;
+                    uint32_t nib = nibble_mask(cand);
+                    parent = (parent & ~nib) | (nib & (r * 0x11111111u));
+                    cols_in |= cand;
+                    uint32_t fr = cand & ~mcols;
+                    if (fr) {
+                        found = __ffs(fr) - 1;
+                        break;
                     }
+                    uint32_t nr = (mc_lo & byte_mask4(cand & 0xFu)) | (mc_hi & byte_mask4(cand >> 4));
+                    nr |= nr >> 16;
+                    nr = (nr | (nr >> 8)) & 0xFFu;
+                    rows_in |= nr;
+                    frontier |= nr;
                 }
                 if (found >= 0) break;
                 // Hall violator: the optimum needs an edge leaving the tree;
@@ -201,14 +220,20 @@ struct Match8 {
                 adj = adjacency(K, L);
                 frontier = rows_in;
             }
-            int c = found;
+            // flip the path back to the root
+            mcols |= 1u << found;
+            uint32_t c = (uint32_t)found;
             for (;;) {
-                int r = (int)get4(parent, c);
+                uint32_t r = get4(parent, c);
                 uint32_t pc = get4(mrow, r);
-                mrow = set4(mrow, r, (uint32_t)c);
-                mcol = set4(mcol, c, (uint32_t)r);
-                if (r == u) break;
-                c = (int)pc;
+                mrow = set4(mrow, r, c);
+                uint32_t sh = 8 * (c & 3), rb = (1u << r) << sh, keep = ~(0xFFu << sh);
+                if (c < 4)
+                    mc_lo = (mc_lo & keep) | rb;
+                else
+                    mc_hi = (mc_hi & keep) | rb;
+                if (r == (uint32_t)u) break;
+                c = pc;
             }
         }
         return L;
