@@ -13,6 +13,7 @@ scaling, no data-path collective); time is the max over ranks.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -114,6 +115,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """fd-level: NCCL prints its version banner with printf at communicator
+    init, whatever NCCL_DEBUG_FILE says; keep rank 0's stdout one JSON line."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -180,7 +196,9 @@ def run_ours():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        with stdout_to_stderr():
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            dist.barrier()
     dev = torch.device(f"cuda:{local}")
     g, w = instance()
     inst = N.instance_for(g, w, local)

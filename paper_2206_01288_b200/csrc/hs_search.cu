@@ -320,6 +320,128 @@ __device__ __forceinline__ void invalidate(LS& s, int j) {
     s.cver[j]++;
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident sweep of one group pair at d_dp = 8, n <= 128.
+//
+// Both groups live in every lane as 8 packed bytes (member i = byte i,
+// ascending).  One _best_candidate round is: each lane prices one intra pair
+// (i, l) of each group, the two lexicographic first minima come out of three
+// REDUX.MIN stages on the order-preserving 64-bit image of the weight (high
+// word, low word, pair code), lanes 4q.. form the four 8-term pairwise row
+// sums of _gain_ours, and the swap is two byte-shifts of the packed words.
+// No shared-memory state changes until the pair settles.
+
+__device__ __forceinline__ uint32_t byte_of(uint64_t x, uint32_t i) {
+    return __byte_perm((uint32_t)x, (uint32_t)(x >> 32), i) & 0xFFu;
+}
+
+__device__ __forceinline__ uint64_t bytes_below(uint32_t c) {  // c in 0..8
+    return c >= 8 ? ~0ull : ((1ull << (8 * c)) - 1ull);
+}
+
+// group x (8 sorted ids) without its member at position p, then with v
+// inserted in order (ids < 128)
+__device__ __forceinline__ uint64_t replace_member(uint64_t x, uint32_t p, uint32_t v) {
+    const uint64_t lowp = bytes_below(p);
+    const uint64_t z = (x & lowp) | ((x >> 8) & ~lowp);  // 7 survivors, byte 7 = 0
+    uint32_t c = 0;
+    if (v) {  // survivors below v: bit 7 of (0x80 + v - 1 - z) per byte
+        const uint64_t t = ((uint64_t)(0x80u + v - 1u) * 0x0101010101010101ull - z) & 0x0080808080808080ull;
+        c = __popcll(t);
+    }
+    const uint64_t lowc = bytes_below(c);
+    return (z & lowc) | ((z << 8) & ~bytes_below(c + 1)) | ((uint64_t)v << (8 * c));
+}
+
+// order-preserving image of a double (no NaN); -0.0 folds onto +0.0 so
+// equal values tie like the reference's `<`
+__device__ __forceinline__ uint64_t ord_bits(double v) {
+    const uint64_t b = (uint64_t)__double_as_longlong(v + 0.0);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// _fast_edge of two packed groups at once; returns codes i*8+l (i < l)
+__device__ __forceinline__ void fast_edges8(const double* W, int n, uint64_t X, uint64_t Y, int lane, uint32_t pi,
+                                            uint32_t pl, uint32_t& cx, uint32_t& cy) {
+    uint64_t kx = ~0ull, ky = ~0ull;
+    if (lane < 28) {
+        kx = ord_bits(W[byte_of(X, pi) * n + byte_of(X, pl)]);
+        ky = ord_bits(W[byte_of(Y, pi) * n + byte_of(Y, pl)]);
+    }
+    const uint32_t hx = (uint32_t)(kx >> 32), hy = (uint32_t)(ky >> 32);
+    const uint32_t mhx = __reduce_min_sync(kFull, hx), mhy = __reduce_min_sync(kFull, hy);
+    const uint32_t lx = hx == mhx ? (uint32_t)kx : 0xFFFFFFFFu, ly = hy == mhy ? (uint32_t)ky : 0xFFFFFFFFu;
+    const uint32_t mlx = __reduce_min_sync(kFull, lx), mly = __reduce_min_sync(kFull, ly);
+    const uint32_t code = pi * 8 + pl;
+    cx = __reduce_min_sync(kFull, (hx == mhx && lx == mlx && lane < 28) ? code : 0xFFu);
+    cy = __reduce_min_sync(kFull, (hy == mhy && ly == mly && lane < 28) ? code : 0xFFu);
+}
+
+// the `for _ in range(d_dp)` loop of _pass_ours for pair (j, j2); true if a
+// swap was applied
+__device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, uint32_t pl) {
+    const int n = s.n;
+    const double* W = s.W;
+    const int16_t* gj = s.G + j * s.cap;
+    const int16_t* gj2 = s.G + j2 * s.cap;
+    uint64_t X = 0, Y = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        X |= (uint64_t)(uint8_t)gj[i] << (8 * i);
+        Y |= (uint64_t)(uint8_t)gj2[i] << (8 * i);
+    }
+    const int q = lane & 3;
+    bool changed = false;
+    for (int it = 0; it < 8; it++) {
+        uint32_t cx, cy;
+        fast_edges8(W, n, X, Y, lane, pi, pl, cx, cy);
+        const uint32_t d1 = byte_of(X, cx >> 3), d2 = byte_of(X, cx & 7);
+        const uint32_t d1p = byte_of(Y, cy >> 3), d2p = byte_of(Y, cy & 7);
+        // lane q: t_q = psum(w[u, other]) / 8 - w[u, partner]  (_gain_ours)
+        const uint32_t u = q == 0 ? d1 : q == 1 ? d2 : q == 2 ? d1p : d2p;
+        const uint32_t pu = q == 0 ? d2 : q == 1 ? d1 : q == 2 ? d2p : d1p;
+        const uint64_t O = q < 2 ? Y : X;
+        const double* wr = W + (size_t)u * n;
+        double r[8];
+#pragma unroll
+        for (int e = 0; e < 8; e++) r[e] = wr[byte_of(O, e)];
+        const double sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        const double t = div_count(sum, 8) - wr[pu];
+        const double t1a = __shfl_sync(kFull, t, 0), t1b = __shfl_sync(kFull, t, 1);
+        const double t2a = __shfl_sync(kFull, t, 2), t2b = __shfl_sync(kFull, t, 3);
+        // _best_candidate: (d1,d1p), (d1,d2p), (d2,d1p), (d2,d2p), first best
+        const double g[4] = {t1a + t2a, t1a + t2b, t1b + t2a, t1b + t2b};
+        double best = -kInf;
+        int bc = 0;
+#pragma unroll
+        for (int c = 0; c < 4; c++)
+            if (g[c] > best) {
+                best = g[c];
+                bc = c;
+            }
+        if (!(best > 0.0)) break;
+        const uint32_t pa = (bc < 2) ? (cx >> 3) : (cx & 7);      // a = d1 or d2 in group j
+        const uint32_t pb = (bc & 1) ? (cy & 7) : (cy >> 3);      // b = d1p or d2p in group j2
+        const uint32_t a = byte_of(X, pa), b = byte_of(Y, pb);
+        X = replace_member(X, pa, b);  // _swap (:252-257)
+        Y = replace_member(Y, pb, a);
+        changed = true;
+    }
+    if (changed) {
+        __syncwarp();
+        int16_t* wj = s.G + j * s.cap;
+        int16_t* wj2 = s.G + j2 * s.cap;
+        if (lane < 8) wj[lane] = (int16_t)byte_of(X, lane);
+        else if (lane < 16) wj2[lane - 8] = (int16_t)byte_of(Y, lane - 8);
+        if (lane == 0) {
+            invalidate(s, j);
+            invalidate(s, j2);
+        }
+        __syncwarp();
+    }
+    return changed;
+}
+
 // even phase of _pass_ours: swap sweep over rng.permutation(C(k,2)) pairs
 __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
     const int k = s.k, np = k * (k - 1) / 2, d_dp = s.sz[0];
@@ -334,9 +456,25 @@ __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
     }
     __syncwarp();
     bool changed = false;
+    // this lane's intra pair (i, l), lexicographic, for the d_dp = 8 path
+    uint32_t pi = 0, pl = 1;
+    if (lane < 28) {
+        int i = 0, t = lane;
+        while (t >= 7 - i) {
+            t -= 7 - i;
+            i++;
+        }
+        pi = (uint32_t)i;
+        pl = (uint32_t)(i + 1 + t);
+    }
+    const bool fast8 = d_dp == 8 && s.n <= 128;
     for (int q = 0; q < np; q++) {
         int j, j2;
         decode_pair(s.perm[q], k, j, j2);
+        if (fast8 && s.sz[j] == 8 && s.sz[j2] == 8) {
+            if (sweep_pair8(s, j, j2, lane, pi, pl)) changed = true;
+            continue;
+        }
         for (int it = 0; it < d_dp; it++) {
             int a, b;
             long long b0 = clock64();
