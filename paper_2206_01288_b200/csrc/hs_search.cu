@@ -669,8 +669,345 @@ __device__ __noinline__ bool chain_round(LS& s, int lane) {
     return applied;
 }
 
+// ---------------------------------------------------------------------------
+// Odd phase of _pass_ours for n <= 64, k <= 8, register resident.
+//
+// Groups are 64-bit membership masks (ascending member order is the bit
+// order), lane j holding group j's; lane l owns devices l and l + 32 (their
+// group and home cost).  The locked set is one uniform mask.  Every mean the
+// chain reads is recomputed from the current masks (a sequential sum over
+// the members, as w[:, grp].mean(axis=1) reduces it), so no mean cache is
+// kept; home costs are refreshed for the groups a move touched.  Minima and
+// maxima with first-index ties are three REDUX stages on the order-preserving
+// image of the double (high word, low word, index).
+
+__device__ __forceinline__ double from_ord(uint64_t k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+}
+
+// min value over valid lanes, smallest idx among equal minima (INT_MAX if none)
+__device__ __forceinline__ int redux_argmin(double v, bool valid, int idx, double& best) {
+    const uint64_t k = valid ? ord_bits(v) : ~0ull;
+    const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+    const uint32_t mh = __reduce_min_sync(kFull, hi);
+    const uint32_t ml = __reduce_min_sync(kFull, hi == mh ? lo : 0xFFFFFFFFu);
+    const int wi = (int)__reduce_min_sync(kFull, (valid && hi == mh && lo == ml) ? (unsigned)idx : 0x7FFFFFFFu);
+    best = from_ord(((uint64_t)mh << 32) | ml);
+    return wi;
+}
+
+// max value over valid lanes, smallest idx among equal maxima (INT_MAX if none)
+__device__ __forceinline__ int redux_argmax(double v, bool valid, int idx, double& best) {
+    const uint64_t k = valid ? ord_bits(v) : 0ull;
+    const uint32_t hi = (uint32_t)(k >> 32), lo = (uint32_t)k;
+    const uint32_t mh = __reduce_max_sync(kFull, hi);
+    const uint32_t ml = __reduce_max_sync(kFull, hi == mh ? lo : 0u);
+    const int wi = (int)__reduce_min_sync(kFull, (valid && hi == mh && lo == ml) ? (unsigned)idx : 0x7FFFFFFFu);
+    best = from_ord(((uint64_t)mh << 32) | ml);
+    return wi;
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t x, int src) {
+    const uint32_t lo = __shfl_sync(kFull, (uint32_t)x, src), hi = __shfl_sync(kFull, (uint32_t)(x >> 32), src);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// A group's members as 16 packed bytes (ascending, 0xFF past the end), held
+// by the group's lane as two 64-bit halves: iteration is byte extraction, a
+// move is a byte shift at the member's rank.
+struct Members {
+    uint64_t lo, hi;
+};
+
+__device__ __forceinline__ uint32_t mbyte(const Members& L, int t) {  // t static after unrolling
+    return (uint32_t)((t < 8 ? L.lo >> (8 * t) : L.hi >> (8 * (t - 8))) & 0xFFu);
+}
+
+__device__ __forceinline__ Members shfl_members(const Members& L, int src) {
+    return Members{shfl64(L.lo, src), shfl64(L.hi, src)};
+}
+
+__device__ __forceinline__ void byte_masks(int p, uint64_t& ml, uint64_t& mh) {  // bytes [0, p), p <= 16
+    ml = p >= 8 ? ~0ull : ((1ull << (8 * p)) - 1ull);
+    mh = p <= 8 ? 0ull : (p >= 16 ? ~0ull : ((1ull << (8 * (p - 8))) - 1ull));
+}
+
+__device__ __forceinline__ void members_remove(Members& L, int p) {
+    uint64_t ml, mh;
+    byte_masks(p, ml, mh);
+    const uint64_t lo_s = (L.lo >> 8) | (L.hi << 56), hi_s = (L.hi >> 8) | (0xFFull << 56);
+    L.lo = (L.lo & ml) | (lo_s & ~ml);
+    L.hi = (L.hi & mh) | (hi_s & ~mh);
+}
+
+__device__ __forceinline__ void members_insert(Members& L, int c, uint32_t v) {
+    uint64_t ml, mh, ml1, mh1;
+    byte_masks(c, ml, mh);
+    byte_masks(c + 1, ml1, mh1);
+    const uint64_t lo_s = L.lo << 8, hi_s = (L.hi << 8) | (L.lo >> 56);
+    L.lo = (L.lo & ml) | (lo_s & ~ml1) | (c < 8 ? (uint64_t)v << (8 * c) : 0ull);
+    L.hi = (L.hi & mh) | (hi_s & ~mh1) | (c >= 8 ? (uint64_t)v << (8 * (c - 8)) : 0ull);
+}
+
+// w[u, grp].mean() over cnt packed members: sequential sum (as numpy reduces
+// the F-contiguous gather), then / count; all loads issued up front
+__device__ __forceinline__ double members_mean(const double* wr, const Members& L, int cnt) {
+    double w[16];
+#pragma unroll
+    for (int t = 0; t < 16; t++) w[t] = t < cnt ? wr[mbyte(L, t)] : 0.0;
+    double r = 0.0;
+#pragma unroll
+    for (int t = 0; t < 16; t++)
+        if (t < cnt) r += w[t];
+    return div_count(r, cnt);
+}
+
+// min of wr over the members other than `self` (order-free), +inf if none
+__device__ __forceinline__ double members_min(const double* wr, const Members& L, int cnt, uint32_t self) {
+    double h = kInf;
+#pragma unroll
+    for (int t = 0; t < 16; t++) {
+        const uint32_t x = mbyte(L, t);
+        if (t < cnt && x != self) h = dmin(h, wr[x]);
+    }
+    return h;
+}
+
+struct ChainRegs {
+    uint64_t GM;        // lane j < k: members of group j (mask)
+    Members L;          // lane j < k: the same members, packed ascending
+    uint64_t locked;    // uniform
+    uint32_t dirty;     // uniform: groups whose home costs are stale
+    int g0, g1;         // groups of this lane's devices (lane, lane + 32); -1 if absent
+    double h0, h1;      // their home costs (valid for unlocked devices in clean groups)
+};
+
+// _move (:294-296): v leaves src for dst (bisect.insort keeps the order)
+__device__ __forceinline__ void cmove(ChainRegs& c, int v, int src, int dst, int lane) {
+    const uint64_t bit = 1ull << v;
+    if (lane == src) {
+        members_remove(c.L, __popcll(c.GM & (bit - 1ull)));
+        c.GM &= ~bit;
+    }
+    if (lane == dst) {
+        members_insert(c.L, __popcll(c.GM & (bit - 1ull)), (uint32_t)v);
+        c.GM |= bit;
+    }
+    if (lane == (v & 31)) {
+        if (v < 32)
+            c.g0 = dst;
+        else
+            c.g1 = dst;
+    }
+    c.dirty |= (1u << src) | (1u << dst);
+}
+
+// _home_costs (:287-291) for this lane's unlocked devices in dirty groups
+__device__ __forceinline__ void refresh_homes(const LS& s, ChainRegs& c, int lane) {
+    if (!c.dirty) return;
+    const int s0 = c.g0 < 0 ? 0 : c.g0, s1 = c.g1 < 0 ? 0 : c.g1;
+    const Members m0 = shfl_members(c.L, s0), m1 = shfl_members(c.L, s1);
+    const int n0 = __popcll(shfl64(c.GM, s0)), n1 = __popcll(shfl64(c.GM, s1));
+    const int n = s.n;
+    const bool r0 = c.g0 >= 0 && (c.dirty >> c.g0 & 1u) && !(c.locked >> lane & 1ull);
+    const bool r1 = c.g1 >= 0 && (c.dirty >> c.g1 & 1u) && !(c.locked >> (lane + 32) & 1ull);
+    if (r0) c.h0 = members_min(s.W + (size_t)lane * n, m0, n0, (uint32_t)lane);
+    if (r1) c.h1 = members_min(s.W + (size_t)(lane + 32) * n, m1, n1, (uint32_t)(lane + 32));
+    c.dirty = 0;
+}
+
+// this lane's best unlocked device of group i by (home, id); false if none
+__device__ __forceinline__ bool lane_free(const ChainRegs& c, int i, int lane, double& h, int& d) {
+    const bool ok0 = c.g0 == i && !(c.locked >> lane & 1ull);
+    const bool ok1 = c.g1 == i && !(c.locked >> (lane + 32) & 1ull);
+    h = (ok0 && !(ok1 && c.h1 < c.h0)) ? c.h0 : c.h1;
+    d = (ok0 && !(ok1 && c.h1 < c.h0)) ? lane : lane + 32;
+    return ok0 || ok1;
+}
+
+// fastest_free (:318-328) of group i: -1 if none
+__device__ __forceinline__ int chain_fastest_free(const ChainRegs& c, int i, int lane, double& home) {
+    const int cnt = __popcll(shfl64(c.GM, i));
+    double h;
+    int d;
+    const bool ok = lane_free(c, i, lane, h, d);
+    const int v = redux_argmin(h, ok, d, home);
+    return (cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
+}
+
+__device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
+    const int k = s.k, n = s.n;
+    refresh_homes(s, c, lane);
+    // fastest_free of every group at once: three REDUX stages, 8 groups wide
+    int vv[8];
+    double hh[8];
+    {
+        uint32_t hi[8], lo[8], mh[8], ml[8];
+        int id[8];
+        bool ok[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            double h;
+            ok[i] = i < k && lane_free(c, i, lane, h, id[i]);
+            const uint64_t key = ok[i] ? ord_bits(h) : ~0ull;
+            hi[i] = (uint32_t)(key >> 32);
+            lo[i] = (uint32_t)key;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) mh[i] = __reduce_min_sync(kFull, hi[i]);
+#pragma unroll
+        for (int i = 0; i < 8; i++) ml[i] = __reduce_min_sync(kFull, hi[i] == mh[i] ? lo[i] : 0xFFFFFFFFu);
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            const int v = (int)__reduce_min_sync(
+                kFull, (ok[i] && hi[i] == mh[i] && lo[i] == ml[i]) ? (unsigned)id[i] : 0x7FFFFFFFu);
+            const int cnt = __popcll(shfl64(c.GM, i & 31));
+            vv[i] = (i >= k || cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
+            hh[i] = from_ord(((uint64_t)mh[i] << 32) | ml[i]);
+        }
+    }
+    // gain_i = max_{j != i} mean[v_i, j] - home_i for (i, j) = (e >> 3, e & 7),
+    // e = lane + 32 sl: row maxima inside 8-lane segments
+    const Members Lj = shfl_members(c.L, lane & 7);
+    const int cj = __popcll(shfl64(c.GM, lane & 7));
+    double gsl[2];
+    int isl[2];
+#pragma unroll
+    for (int sl = 0; sl < 2; sl++) {
+        const int i = (lane >> 3) + 4 * sl, j = lane & 7;
+        int vi = -1;
+        double hi = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (q == i) {
+                vi = vv[q];
+                hi = hh[q];
+            }
+        double x = -kInf;
+        if (j < k && j != i && vi >= 0) x = members_mean(s.W + (size_t)vi * n, Lj, cj);
+        x = dmax(x, __shfl_xor_sync(kFull, x, 1));
+        x = dmax(x, __shfl_xor_sync(kFull, x, 2));
+        x = dmax(x, __shfl_xor_sync(kFull, x, 4));
+        gsl[sl] = x - hi;
+        isl[sl] = (vi >= 0 && j == 0) ? i : -1;
+    }
+    // first strict maximum over i from best_start = -inf
+    const bool u0 = isl[0] >= 0 && gsl[0] > -kInf, u1 = isl[1] >= 0 && gsl[1] > -kInf;
+    const bool take1 = u1 && (!u0 || gsl[1] > gsl[0]);
+    double best;
+    const int start0 = redux_argmax(take1 ? gsl[1] : gsl[0], u0 || u1, take1 ? isl[1] : isl[0], best);
+    if (start0 == 0x7FFFFFFF) return false;
+    const int start = start0;
+    int* mv_v = s.i32;
+    int* mv_src = s.i32 + k;
+    int* mv_dst = s.i32 + 2 * k;
+    double* steps = s.f64;
+    double* closers = s.f64 + k + 1;
+    int cur = start, nm = 0;
+    bool natural = false;
+    for (int it = 0; it < k; it++) {
+        refresh_homes(s, c, lane);
+        double home;
+        const int v = chain_fastest_free(c, cur, lane, home);
+        if (v < 0) break;
+        // scores = mean[v, targets]; dst = first maximum
+        double mj = 0.0;
+        if (lane < k) mj = members_mean(s.W + (size_t)v * n, c.L, __popcll(c.GM));
+        double sc;
+        const int dst = redux_argmax(mj, lane < k && lane != cur, lane, sc);
+        const double mstart = __shfl_sync(kFull, mj, start);
+        if (lane == 0) {
+            closers[nm] = cur != start ? mstart - home : -kInf;
+            steps[nm] = sc - home;
+            mv_v[nm] = v;
+            mv_src[nm] = cur;
+            mv_dst[nm] = dst;
+        }
+        c.locked |= 1ull << v;
+        cmove(c, v, cur, dst, lane);
+        nm++;
+        cur = dst;
+        if (cur == start) {
+            natural = true;
+            break;
+        }
+    }
+    __syncwarp();
+    double prefix = 0.0, best_v = -kInf;
+    int best_l = -1;
+    for (int l = 0; l < nm; l++) {  // prefix[l] = cumsum of steps[0..l-1]
+        const double value = prefix + closers[l];
+        if (value > best_v) {
+            best_v = value;
+            best_l = l;
+        }
+        prefix = prefix + steps[l];
+    }
+    if (natural && prefix > best_v) {
+        best_v = prefix;
+        best_l = nm;
+    }
+    const bool applied = best_v > 0.0;
+    const int keep = applied ? best_l : 0;
+    for (int t = nm - 1; t >= keep; t--) cmove(c, mv_v[t], mv_dst[t], mv_src[t], lane);
+    if (applied && best_l < nm) cmove(c, mv_v[best_l], mv_src[best_l], start, lane);
+    __syncwarp();
+    return applied;
+}
+
+__device__ bool pass_chains8(LS& s, int lane) {
+    const int k = s.k, n = s.n;
+    ChainRegs c;
+    c.GM = 0;
+    c.L = Members{~0ull, ~0ull};
+    if (lane < k) {
+        const int16_t* g = s.G + lane * s.cap;
+        for (int t = 0; t < s.sz[lane]; t++) {
+            c.GM |= 1ull << g[t];
+            if (t < 8)
+                c.L.lo = (c.L.lo & ~(0xFFull << (8 * t))) | ((uint64_t)g[t] << (8 * t));
+            else
+                c.L.hi = (c.L.hi & ~(0xFFull << (8 * (t - 8)))) | ((uint64_t)g[t] << (8 * (t - 8)));
+        }
+    }
+    c.g0 = c.g1 = -1;
+    for (int j = 0; j < k; j++) {
+        const uint64_t m = shfl64(c.GM, j);
+        if (m >> lane & 1ull) c.g0 = j;
+        if (lane + 32 < n && (m >> (lane + 32) & 1ull)) c.g1 = j;
+    }
+    c.h0 = c.h1 = kInf;
+    c.locked = 0;
+    c.dirty = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
+    const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+    bool changed = false;
+    while (c.locked != all) {
+        const uint64_t before = c.locked;
+        if (chain_round8(s, c, lane)) changed = true;
+        if (c.locked == before) break;
+    }
+    // back to sorted member lists; every cache of the touched groups is stale
+    __syncwarp();
+    if (lane < k) {
+        const int cnt = __popcll(c.GM);
+        int16_t* g = s.G + lane * s.cap;
+#pragma unroll
+        for (int t = 0; t < 16; t++)
+            if (t < cnt) g[t] = (int16_t)mbyte(c.L, t);
+        s.sz[lane] = cnt;
+        s.cver[lane]++;
+    }
+    if (lane == 0) {
+        s.valid[1] = 0;
+        s.valid[2] = 0;
+    }
+    __syncwarp();
+    return changed;
+}
+
 // odd phase of _pass_ours: chains until every device is locked
 __device__ __noinline__ bool pass_chains(LS& s, int lane) {
+    if (s.n <= 64 && s.k <= 8 && s.m <= 15) return pass_chains8(s, lane);
     const int n = s.n;
     for (int i = lane; i < ((n + 31) >> 5); i += kWarp) s.locked[i] = 0;
     if (lane == 0) s.nlocked[0] = 0;

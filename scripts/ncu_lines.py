@@ -35,7 +35,7 @@ for f in os.listdir(tmp):
         m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
         if m and cur:
             addr2line[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
+out = subprocess.run(["ncu", "-i", rep, *os.environ.get("NCU_FILTER", "").split(), "--page", "source", "--csv", "--print-source=sass"], capture_output=True,
                      text=True).stdout.splitlines()
 rows = list(csv.reader(out))
 hdr = None
