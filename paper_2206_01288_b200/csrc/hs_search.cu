@@ -751,22 +751,24 @@ __device__ __forceinline__ void members_insert(Members& L, int c, uint32_t v) {
 
 // w[u, grp].mean() over cnt packed members: sequential sum (as numpy reduces
 // the F-contiguous gather), then / count; all loads issued up front
+template <int MAXC>
 __device__ __forceinline__ double members_mean(const double* wr, const Members& L, int cnt) {
-    double w[16];
+    double w[MAXC];
 #pragma unroll
-    for (int t = 0; t < 16; t++) w[t] = t < cnt ? wr[mbyte(L, t)] : 0.0;
+    for (int t = 0; t < MAXC; t++) w[t] = t < cnt ? wr[mbyte(L, t)] : 0.0;
     double r = 0.0;
 #pragma unroll
-    for (int t = 0; t < 16; t++)
+    for (int t = 0; t < MAXC; t++)
         if (t < cnt) r += w[t];
     return div_count(r, cnt);
 }
 
 // min of wr over the members other than `self` (order-free), +inf if none
+template <int MAXC>
 __device__ __forceinline__ double members_min(const double* wr, const Members& L, int cnt, uint32_t self) {
     double h = kInf;
 #pragma unroll
-    for (int t = 0; t < 16; t++) {
+    for (int t = 0; t < MAXC; t++) {
         const uint32_t x = mbyte(L, t);
         if (t < cnt && x != self) h = dmin(h, wr[x]);
     }
@@ -777,13 +779,15 @@ struct ChainRegs {
     uint64_t GM;        // lane j < k: members of group j (mask)
     Members L;          // lane j < k: the same members, packed ascending
     uint64_t locked;    // uniform
-    uint32_t dirty;     // uniform: groups whose home costs are stale
     int g0, g1;         // groups of this lane's devices (lane, lane + 32); -1 if absent
-    double h0, h1;      // their home costs (valid for unlocked devices in clean groups)
+    double h0, h1;      // their home costs (kept for unlocked devices)
+    bool st0, st1;      // home cost must be recomputed
 };
 
-// _move (:294-296): v leaves src for dst (bisect.insort keeps the order)
-__device__ __forceinline__ void cmove(ChainRegs& c, int v, int src, int dst, int lane) {
+// _move (:294-296): v leaves src for dst (bisect.insort keeps the order).
+// Home costs follow exactly (min is order-free): a member of dst takes
+// min(home, w[d, v]); a member of src keeps its home unless v was at it.
+__device__ __forceinline__ void cmove(const LS& s, ChainRegs& c, int v, int src, int dst, int lane) {
     const uint64_t bit = 1ull << v;
     if (lane == src) {
         members_remove(c.L, __popcll(c.GM & (bit - 1ull)));
@@ -793,27 +797,47 @@ __device__ __forceinline__ void cmove(ChainRegs& c, int v, int src, int dst, int
         members_insert(c.L, __popcll(c.GM & (bit - 1ull)), (uint32_t)v);
         c.GM |= bit;
     }
-    if (lane == (v & 31)) {
-        if (v < 32)
-            c.g0 = dst;
-        else
-            c.g1 = dst;
+    const int d0 = lane, d1 = lane + 32;
+    if (d0 == v) {
+        c.g0 = dst;
+        c.st0 = true;
+    } else if ((c.g0 == src || c.g0 == dst) && !(c.locked >> d0 & 1ull) && !c.st0) {
+        const double w = s.W[(size_t)d0 * s.n + v];
+        if (c.g0 == dst)
+            c.h0 = dmin(c.h0, w);
+        else if (!(w > c.h0))
+            c.st0 = true;
     }
-    c.dirty |= (1u << src) | (1u << dst);
+    if (d1 == v) {
+        c.g1 = dst;
+        c.st1 = true;
+    } else if ((c.g1 == src || c.g1 == dst) && !(c.locked >> d1 & 1ull) && !c.st1) {
+        const double w = s.W[(size_t)d1 * s.n + v];
+        if (c.g1 == dst)
+            c.h1 = dmin(c.h1, w);
+        else if (!(w > c.h1))
+            c.st1 = true;
+    }
 }
 
-// _home_costs (:287-291) for this lane's unlocked devices in dirty groups
+// _home_costs (:287-291) for this lane's unlocked devices with a stale home
+template <int MAXC>
 __device__ __forceinline__ void refresh_homes(const LS& s, ChainRegs& c, int lane) {
-    if (!c.dirty) return;
+    const bool r0 = c.st0 && c.g0 >= 0 && !(c.locked >> lane & 1ull);
+    const bool r1 = c.st1 && c.g1 >= 0 && !(c.locked >> (lane + 32) & 1ull);
+    if (!__any_sync(kFull, r0 || r1)) return;
     const int s0 = c.g0 < 0 ? 0 : c.g0, s1 = c.g1 < 0 ? 0 : c.g1;
     const Members m0 = shfl_members(c.L, s0), m1 = shfl_members(c.L, s1);
     const int n0 = __popcll(shfl64(c.GM, s0)), n1 = __popcll(shfl64(c.GM, s1));
     const int n = s.n;
-    const bool r0 = c.g0 >= 0 && (c.dirty >> c.g0 & 1u) && !(c.locked >> lane & 1ull);
-    const bool r1 = c.g1 >= 0 && (c.dirty >> c.g1 & 1u) && !(c.locked >> (lane + 32) & 1ull);
-    if (r0) c.h0 = members_min(s.W + (size_t)lane * n, m0, n0, (uint32_t)lane);
-    if (r1) c.h1 = members_min(s.W + (size_t)(lane + 32) * n, m1, n1, (uint32_t)(lane + 32));
-    c.dirty = 0;
+    if (r0) {
+        c.h0 = members_min<MAXC>(s.W + (size_t)lane * n, m0, n0, (uint32_t)lane);
+        c.st0 = false;
+    }
+    if (r1) {
+        c.h1 = members_min<MAXC>(s.W + (size_t)(lane + 32) * n, m1, n1, (uint32_t)(lane + 32));
+        c.st1 = false;
+    }
 }
 
 // this lane's best unlocked device of group i by (home, id); false if none
@@ -835,9 +859,10 @@ __device__ __forceinline__ int chain_fastest_free(const ChainRegs& c, int i, int
     return (cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
 }
 
+template <int MAXC>
 __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     const int k = s.k, n = s.n;
-    refresh_homes(s, c, lane);
+    refresh_homes<MAXC>(s, c, lane);
     // fastest_free of every group at once: three REDUX stages, 8 groups wide
     int vv[8];
     double hh[8];
@@ -884,7 +909,7 @@ __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
                 hi = hh[q];
             }
         double x = -kInf;
-        if (j < k && j != i && vi >= 0) x = members_mean(s.W + (size_t)vi * n, Lj, cj);
+        if (j < k && j != i && vi >= 0) x = members_mean<MAXC>(s.W + (size_t)vi * n, Lj, cj);
         x = dmax(x, __shfl_xor_sync(kFull, x, 1));
         x = dmax(x, __shfl_xor_sync(kFull, x, 2));
         x = dmax(x, __shfl_xor_sync(kFull, x, 4));
@@ -906,13 +931,13 @@ __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     int cur = start, nm = 0;
     bool natural = false;
     for (int it = 0; it < k; it++) {
-        refresh_homes(s, c, lane);
+        refresh_homes<MAXC>(s, c, lane);
         double home;
         const int v = chain_fastest_free(c, cur, lane, home);
         if (v < 0) break;
         // scores = mean[v, targets]; dst = first maximum
         double mj = 0.0;
-        if (lane < k) mj = members_mean(s.W + (size_t)v * n, c.L, __popcll(c.GM));
+        if (lane < k) mj = members_mean<MAXC>(s.W + (size_t)v * n, c.L, __popcll(c.GM));
         double sc;
         const int dst = redux_argmax(mj, lane < k && lane != cur, lane, sc);
         const double mstart = __shfl_sync(kFull, mj, start);
@@ -924,7 +949,7 @@ __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
             mv_dst[nm] = dst;
         }
         c.locked |= 1ull << v;
-        cmove(c, v, cur, dst, lane);
+        cmove(s, c, v, cur, dst, lane);
         nm++;
         cur = dst;
         if (cur == start) {
@@ -949,12 +974,13 @@ __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     }
     const bool applied = best_v > 0.0;
     const int keep = applied ? best_l : 0;
-    for (int t = nm - 1; t >= keep; t--) cmove(c, mv_v[t], mv_dst[t], mv_src[t], lane);
-    if (applied && best_l < nm) cmove(c, mv_v[best_l], mv_src[best_l], start, lane);
+    for (int t = nm - 1; t >= keep; t--) cmove(s, c, mv_v[t], mv_dst[t], mv_src[t], lane);
+    if (applied && best_l < nm) cmove(s, c, mv_v[best_l], mv_src[best_l], start, lane);
     __syncwarp();
     return applied;
 }
 
+template <int MAXC>
 __device__ bool pass_chains8(LS& s, int lane) {
     const int k = s.k, n = s.n;
     ChainRegs c;
@@ -977,13 +1003,13 @@ __device__ bool pass_chains8(LS& s, int lane) {
         if (lane + 32 < n && (m >> (lane + 32) & 1ull)) c.g1 = j;
     }
     c.h0 = c.h1 = kInf;
+    c.st0 = c.st1 = true;
     c.locked = 0;
-    c.dirty = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
     const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
     bool changed = false;
     while (c.locked != all) {
         const uint64_t before = c.locked;
-        if (chain_round8(s, c, lane)) changed = true;
+        if (chain_round8<MAXC>(s, c, lane)) changed = true;
         if (c.locked == before) break;
     }
     // back to sorted member lists; every cache of the touched groups is stale
@@ -992,7 +1018,7 @@ __device__ bool pass_chains8(LS& s, int lane) {
         const int cnt = __popcll(c.GM);
         int16_t* g = s.G + lane * s.cap;
 #pragma unroll
-        for (int t = 0; t < 16; t++)
+        for (int t = 0; t < MAXC; t++)
             if (t < cnt) g[t] = (int16_t)mbyte(c.L, t);
         s.sz[lane] = cnt;
         s.cver[lane]++;
@@ -1007,7 +1033,8 @@ __device__ bool pass_chains8(LS& s, int lane) {
 
 // odd phase of _pass_ours: chains until every device is locked
 __device__ __noinline__ bool pass_chains(LS& s, int lane) {
-    if (s.n <= 64 && s.k <= 8 && s.m <= 15) return pass_chains8(s, lane);
+    if (s.n <= 64 && s.k <= 8 && s.m <= 8) return pass_chains8<9>(s, lane);
+    if (s.n <= 64 && s.k <= 8 && s.m <= 15) return pass_chains8<16>(s, lane);
     const int n = s.n;
     for (int i = lane; i < ((n + 31) >> 5); i += kWarp) s.locked[i] = 0;
     if (lane == 0) s.nlocked[0] = 0;
