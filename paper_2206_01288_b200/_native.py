@@ -45,8 +45,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
     cus = sorted((PKG / "csrc").glob("*.cu"))
 
+    def deps(cu: Path) -> set:
+        """cu plus the local headers it includes, transitively."""
+        seen, todo = set(), [cu]
+        while todo:
+            f = todo.pop()
+            if f in seen or not f.exists():
+                continue
+            seen.add(f)
+            for ln in f.read_text().splitlines():
+                ln = ln.strip()
+                if ln.startswith('#include "'):
+                    name = ln.split('"')[1]
+                    for base in (f.parent, PKG.parent / "include"):
+                        if (base / name).exists():
+                            todo.append(base / name)
+                            break
+        return seen
+
     def one(cu: Path):
         obj = objdir / (cu.stem + ".o")
+        if not force and obj.exists() and obj.stat().st_mtime >= max(d.stat().st_mtime for d in deps(cu)):
+            return obj, subprocess.CompletedProcess([], 0, "", "")
         r = subprocess.run([nvcc, *compile_flags, "-c", "-o", str(obj), str(cu)], capture_output=not verbose,
                            text=True)
         return obj, r
