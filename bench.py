@@ -280,6 +280,15 @@ def run_ours():
     achieved = SMEM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = SMEM_BYTES_PER_CLK_SM * sms * sm_mhz * 1e6 / 1e9
+    traffic, traffic_src, smem_wf = None, None, None
+    tp = ROOT / "profiles" / "eval_traffic.json"
+    if tp.exists():  # ncu --set full capture of this kernel (scripts/gpu_ncu.sh)
+        tj = json.loads(tp.read_text())
+        traffic = tj["dram_bytes_per_launch"] * P / tj["population"]
+        smem_wf = tj["smem_wavefronts_per_launch"] * 128 * P / tj["population"]
+        traffic_src = (f"{tj['source']}: dram__bytes_read.sum + dram__bytes_write.sum at P={tj['population']}"
+                       + ("" if tj["population"] == P else f", scaled to P={P}")
+                       + f"; algorithmic HBM bytes per launch = {HBM_BYTES_PER_EVAL * P}")
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": ARGS.steps,
         "warmup": ARGS.warmup, "ms_per_step": t_ms / ARGS.steps, "higher_is_better": True, "scaling": "weak",
@@ -289,7 +298,8 @@ def run_ours():
                    "l2": f"{nbuf} rotating input populations of {P * 128 / 2**20:.0f} MiB (> 126 MB L2)",
                    "parallelism": f"population sharded over {world} GPU(s), no data-path collective"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "smem_wavefront_bytes": smem_wf,
                      "per_eval_bytes": SMEM_BYTES_PER_EVAL, "kernel": "eval_warp_kernel", "kernel_ms": kern_ms,
                      "peak_source": f"architectural 128 B/clk/SM x {sms} SMs at the {sm_mhz:.0f} MHz SM clock "
                                     "sampled during this run (MEASURED_PEAKS.json has no smem figure)",
@@ -308,6 +318,16 @@ def run_ours():
         line["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads, "kind": "port",
                                 "sample": f"{count} random 8x8 case-{ARGS.case} layouts in {dt:.1f} s "
                                           f"(C oracle restatement of comm_cost, {threads} threads)"}
+        if "ga" in line:
+            # the same 1000-generation evolve through the C oracle port on one
+            # host core (the GA is one sequential chain of generations)
+            o = O.Oracle.of(g, w)
+            t0 = time.perf_counter()
+            ref = o.evolve(64, 1000, "ours", seed=0)
+            t_cpu = time.perf_counter() - t0
+            line["ga"]["time_to_converge"]["cpu_baseline"] = {
+                "seconds": t_cpu, "cores": 1, "kind": "port",
+                "same_best_total": bool(float(ref["total"]) == line["ga"]["time_to_converge"]["best_total_s"])}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -9,6 +9,7 @@ copies the launch csv to profiles/TAG_launches.csv.
 import collections
 import csv
 import io
+import json
 import os
 import shutil
 import subprocess
@@ -111,6 +112,21 @@ if os.path.exists(rp):
                   "| reason | ratio |", "|---|---:|"]
         lines += [f"| {n} | {v:.3f} |" for v, n in sorted(st, reverse=True)]
         lines.append("")
+        if "eval_warp_kernel" in name and os.environ.get("POP"):
+            # per-launch DRAM traffic of the fitness kernel, read by bench.py
+            # for roofline.traffic (bytes per launch at population POP)
+            def num(key, scale):
+                unit, val = rec[key]
+                return float(val) * scale.get(unit, 1.0)
+            byte_units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            dram = num("dram__bytes_read.sum", byte_units) + num("dram__bytes_write.sum", byte_units)
+            json.dump({"tag": tag, "kernel": name, "population": int(os.environ["POP"]),
+                       "dram_bytes_per_launch": dram,
+                       "smem_wavefronts_per_launch": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", {}),
+                       "warp_instructions_per_launch": num("smsp__inst_executed.sum", {}) if "smsp__inst_executed.sum" in rec else None,
+                       "duration_ms": num("gpu__time_duration.sum", {"ms": 1.0, "us": 1e-3, "ns": 1e-6}),
+                       "source": f"profiles/{tag}_ncu.md (ncu --set full --clock-control none, one launch)"},
+                      open(os.path.join(ROOT, "profiles", "eval_traffic.json"), "w"), indent=1)
 os.makedirs(os.path.dirname(out_md), exist_ok=True)
 open(out_md, "w").write("\n".join(lines) + "\n")
 print(out_md)
