@@ -415,11 +415,13 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     CK(cudaStreamSynchronize(h->cs[0]), "sync");
     hs::EvalArgs a = base_args(h);
     a.invalid = h->cinv;
-    int64_t nchunks = (P + h->chunk - 1) / h->chunk;
-    for (int64_t c = 0; c < nchunks; c++) {
+    // double-buffered chunks on two streams; the first chunk is small so the
+    // only copy not hidden behind a kernel is short
+    int64_t lo = 0;
+    for (int64_t c = 0; lo < P; c++) {
         int b = (int)(c & 1);
         cudaStream_t s = h->cs[b];
-        int64_t lo = c * h->chunk, cnt = std::min<int64_t>(h->chunk, P - lo);
+        int64_t cnt = std::min<int64_t>(c == 0 ? h->chunk / 8 : h->chunk, P - lo);
         CK(cudaMemcpyAsync(h->cg[b], groups + lo * km, (size_t)cnt * km * 2, cudaMemcpyHostToDevice, s), "H2D");
         a.groups = h->cg[b];
         a.P = cnt;
@@ -436,6 +438,7 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
             CK(cudaMemcpyAsync(per_group + lo * h->k, a.per_group, (size_t)cnt * h->k * 8, cudaMemcpyDeviceToHost, s),
                "D2H");
         if (order) CK(cudaMemcpyAsync(order + lo * h->k, a.order, (size_t)cnt * h->k, cudaMemcpyDeviceToHost, s), "D2H");
+        lo += cnt;
     }
     CK(cudaStreamSynchronize(h->cs[0]), "sync");
     CK(cudaStreamSynchronize(h->cs[1]), "sync");
