@@ -254,3 +254,52 @@ def test_warp_island_mode_equals_cta_mode(kind):
     b.run(cfg.generations)
     ra, rb = a.results(), b.results()
     assert [r.to_dict() for r in ra] == [r.to_dict() for r in rb]
+
+
+# Shapes around the register-resident driver paths: the d_dp = 8 sweep
+# (n <= 128) and the chain rounds (n <= 64, k <= 8; 9- or 16-member unrolls),
+# plus shapes that fall back to the shared-memory driver on either side.
+DRIVER_SHAPES = [(32, 4, 8), (48, 6, 8), (48, 4, 12), (60, 5, 12), (45, 3, 15), (64, 4, 16), (64, 2, 32),
+                 (96, 12, 8), (128, 16, 8), (40, 8, 5), (24, 8, 3)]
+
+
+def _two_level(n, k):
+    # few distinct weights (tie-heavy, like the preset data-centre cases)
+    from paper_2206_01288_b200.netmodel import scenario_from_ms_gbps
+    size = n // k
+    return scenario_from_ms_gbps([(size, 0.1, 100.0)] * k, 0.25, 25.0, 0).graph()
+
+
+@pytest.mark.parametrize("n,k,m", DRIVER_SHAPES)
+@pytest.mark.parametrize("ties", [False, True])
+def test_evolve_driver_shapes_vs_oracle(n, k, m, ties):
+    """evolve (ours) through the register driver paths reproduces the oracle."""
+    from paper_2206_01288_b200.netmodel import random_graph
+    from paper_2206_01288_b200.workload import WorkloadSpec
+    g = _two_level(n, k) if ties else random_graph(11 + n + k, n)
+    w = WorkloadSpec(k, m, 1 << 30, 3 << 26)
+    pop, gens = (8, 6) if k > 8 else (12, 25)
+    cfg = S.ScheduleConfig(pop_size=pop, generations=gens, local_search="ours", seed=5)
+    r = S.evolve(g, w, cfg)
+    o = O.Oracle.of(g, w).evolve(pop, gens, "ours", seed=5)
+    assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+    assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+    assert [t[1] for t in r.trace] == list(o["trace_best"])
+    assert [t[2] for t in r.trace] == list(o["trace_mean"])
+
+
+@pytest.mark.parametrize("n,k,m", [(32, 4, 8), (48, 4, 12), (64, 8, 8), (128, 16, 8)])
+def test_local_search_driver_shapes_vs_oracle(n, k, m):
+    """local_search (ours) from random starts, RNG stream included."""
+    from paper_2206_01288_b200.netmodel import random_graph
+    from paper_2206_01288_b200.workload import WorkloadSpec
+    g = random_graph(3 * n + k, n)
+    w = WorkloadSpec(k, m, 1 << 30, 3 << 26)
+    rng = np.random.default_rng(n)
+    for t in range(4):
+        p = S.random_partition(rng, n, k, m)
+        r1 = np.random.default_rng(90 + t)
+        st = O.rng_state(np.random.default_rng(90 + t))
+        out = S.local_search(g, w, p, kind="ours", rng=r1)
+        want = O.Oracle.of(g, w).local_search(np.array(p.groups, dtype=np.int32), "ours", st)
+        assert [list(x) for x in out.groups] == want.tolist()
