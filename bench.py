@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-ga", action="store_true", help="skip the GA time-to-converge / island legs")
     ap.add_argument("--islands", type=int, default=0, help="GA islands per GPU (default: 8 per SM, one per warp)")
     ap.add_argument("--island-gens", type=int, default=100)
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the BASELINE config 3-5 legs (scenario / population sweep, 512 and 1024 devices)")
     return ap.parse_args()
 
 
@@ -311,6 +313,8 @@ def run_ours():
     }
     if not ARGS.no_ga:
         line["ga"] = ga_legs(g, w, rank, world, local, barrier, dist)
+    if not ARGS.no_sweep and world == 1:
+        line["other_configs"] = sweep_legs(local)
     if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
         from oracle import oracle as O
         threads = O.cpu_count()
@@ -382,6 +386,81 @@ def ga_legs(g, w, rank, world, local, barrier, dist):
                       "island_generations_per_s": I * world * ARGS.island_gens / t_isl,
                       "mode": "one warp per island (8 per CTA), case-5, pop 64, ours",
                       "migration": "2 elites every 25 generations, global ring, NCCL all-gather"}
+    return out
+
+
+def sweep_legs(local):
+    """Device-resident evals/s on the other BASELINE configs (reported beside
+    the headline, not as bench lines): config 3 = the five paper scenarios
+    at N=64 8x8 over a population sweep; config 4 = 512 devices, 16x32
+    (CTA Held-Karp over 2^16 subsets); config 5 = 1024 devices, 16x64 exact
+    and 32x32 heuristic pricing, plus one gains-only refinement pass per
+    layout (_pass_ours sweep / chains and _pass_kl) on 32x32 groups."""
+    import torch
+    from paper_2206_01288_b200 import PAPER_WORKLOAD, scenario_case
+    from paper_2206_01288_b200 import _native as N
+    from paper_2206_01288_b200 import scheduler as S
+    from paper_2206_01288_b200.netmodel import config4_scenario, random_graph
+    from paper_2206_01288_b200.workload import WorkloadSpec
+
+    dev = torch.device(f"cuda:{local}")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77)
+
+    def layouts(P, n, k, m):
+        perm = torch.argsort(torch.rand((P, n), device=dev, generator=gen), dim=1).to(torch.int16).view(P, k, m)
+        return torch.sort(perm, dim=2).values.contiguous()
+
+    def rate(g, w, P, reps=3, heuristic=False):
+        """device-resident evals/s through hs_eval_batch_ex (CUDA events)"""
+        x = layouts(P, g.lat.shape[0], w.d_pp, w.d_dp)
+        inst = N.instance_for(g, w, local)
+        o = [torch.empty(P, dtype=torch.float64, device=dev) for _ in range(3)]
+        pg = torch.empty((P, w.d_pp), dtype=torch.float64, device=dev)
+        od = torch.empty((P, w.d_pp), dtype=torch.int8, device=dev)
+        sp = torch.cuda.current_stream(dev).cuda_stream
+
+        def call():
+            N.check(N.lib().hs_eval_batch_ex(inst.handle, x.data_ptr(), P, o[0].data_ptr(), o[1].data_ptr(),
+                                             o[2].data_ptr(), pg.data_ptr() if heuristic else None,
+                                             od.data_ptr() if heuristic else None, None, int(heuristic), sp),
+                    "hs_eval_batch_ex")
+        call()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            call()
+        b.record()
+        torch.cuda.synchronize(dev)
+        return P * reps / (a.elapsed_time(b) / 1000.0)
+
+    out = {"config3_scenarios_evals_per_s": {}}
+    for c in range(1, 6):
+        g = scenario_case(c).graph()
+        out["config3_scenarios_evals_per_s"][f"case{c}"] = {
+            str(P): rate(g, PAPER_WORKLOAD, P) for P in (1 << 10, 1 << 14, 1 << 18, 1 << 20)}
+    g4 = config4_scenario().graph()
+    w4 = WorkloadSpec(16, 32, 268_435_456, 201_326_592)
+    out["config4_512dev_16x32_evals_per_s"] = rate(g4, w4, 2048, reps=2)
+    g5 = random_graph(0, 1024)
+    out["config5_1024dev_16x64_evals_per_s"] = rate(g5, WorkloadSpec(16, 64, 1 << 30, 3 << 26), 1024, reps=2)
+    out["config5_1024dev_32x32_heuristic_evals_per_s"] = rate(g5, WorkloadSpec(32, 32, 1 << 30, 3 << 26), 4096,
+                                                              reps=2, heuristic=True)
+    w5 = WorkloadSpec(32, 32, 1 << 30, 3 << 26)
+    inst = N.instance_for(g5, w5, local)
+    B = 1024
+    parts = np.ascontiguousarray(layouts(B, 1024, 32, 32).cpu().numpy())
+    res = np.empty_like(parts)
+    ch = np.zeros(B, dtype=np.int32)
+    passes = {}
+    for name, kind, phase in (("ours_sweep", 0, 0), ("ours_chains", 0, 1), ("kl", 1, 0)):
+        st = S._states([np.random.default_rng(i) for i in range(B)])
+        t0 = time.perf_counter()
+        N.check(N.lib().hs_refine_pass(inst.handle, kind, phase, B, parts.ctypes.data, st, res.ctypes.data,
+                                       ch.ctypes.data), "hs_refine_pass")
+        passes[name] = B / (time.perf_counter() - t0)
+    out["config5_1024dev_32x32_gains_only_passes_per_s"] = passes
     return out
 
 
