@@ -5,6 +5,7 @@
 #include <thrust/unique.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -222,8 +223,52 @@ static hs::EvalArgs base_args(const hs_instance* h) {
     return a;
 }
 
+// d_pp 9..16 without stage order: chunks of stage kernel -> cluster Held-Karp.
+// The stage kernel of chunk c+1 runs on a side stream while the Held-Karp
+// kernel of chunk c runs on `s` (the stage CTAs fit beside the cluster CTAs'
+// shared memory); ping-pong stage buffers, event-ordered.
+static int launch_two(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
+    const bool m8 = a.key16 && a.m == 8 && a.nvals <= 0x8000;
+    if (!h->two_E[set][0]) {
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMalloc(&h->two_E[set][i], (size_t)h->two_chunk * hs::kStageStride * 8), "cudaMalloc stage graphs");
+            CK(cudaMalloc(&h->two_dp[set][i], (size_t)h->two_chunk * 8), "cudaMalloc stage datap");
+            CK(cudaMalloc(&h->two_bad[set][i], (size_t)h->two_chunk), "cudaMalloc stage flags");
+            CK(cudaEventCreateWithFlags(&h->two_ev_stage[set][i], cudaEventDisableTiming), "event");
+            CK(cudaEventCreateWithFlags(&h->two_ev_hk[set][i], cudaEventDisableTiming), "event");
+        }
+        CK(cudaStreamCreateWithFlags(&h->two_side[set], cudaStreamNonBlocking), "stream");
+        CK(cudaEventCreateWithFlags(&h->two_ev_in[set], cudaEventDisableTiming), "event");
+    }
+    cudaStream_t side = h->two_side[set];
+    CK(cudaEventRecord(h->two_ev_in[set], s), "event");  // inputs produced on s before this call
+    CK(cudaStreamWaitEvent(side, h->two_ev_in[set], 0), "wait");
+    int64_t c = 0;
+    for (int64_t lo = 0; lo < a.P; lo += h->two_chunk, c++) {
+        const int i = (int)(c & 1);
+        const int64_t cnt = std::min<int64_t>(h->two_chunk, a.P - lo);
+        hs::EvalArgs ca = a;
+        ca.groups = a.groups + lo * a.k * a.m;
+        ca.P = cnt;
+        ca.datap = a.datap ? a.datap + lo : nullptr;
+        ca.per_group = a.per_group ? a.per_group + lo * a.k : nullptr;
+        if (c >= 2) CK(cudaStreamWaitEvent(side, h->two_ev_hk[set][i], 0), "wait");  // buffer i is free again
+        if (hs::launch_stage(ca, h->two_E[set][i], h->two_dp[set][i], h->two_bad[set][i], h->stage_blocks, m8, side))
+            return hsx::fail(-1, "stage launch", cudaGetLastError());
+        CK(cudaEventRecord(h->two_ev_stage[set][i], side), "event");
+        CK(cudaStreamWaitEvent(s, h->two_ev_stage[set][i], 0), "wait");
+        if (hs::launch_hk_cluster(h->two_E[set][i], hs::kStageES, hs::kStageStride, a.k, cnt, h->two, h->two_grid,
+                                  h->two_dp[set][i], h->two_bad[set][i], a.total + lo, a.pipe ? a.pipe + lo : nullptr,
+                                  s))
+            return hsx::fail(-1, "cluster Held-Karp launch", cudaGetLastError());
+        CK(cudaEventRecord(h->two_ev_hk[set][i], s), "event");
+    }
+    return 0;
+}
+
 static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
     if (h->k > 16) return hsx::fail(-3, "exact pricing is limited to d_pp <= 16 (Held-Karp); use heuristic paths");
+    if (h->k > hs::kWarpK && !a.order && h->two.tasks) return launch_two(h, a, set, s);
     if (h->k > hs::kWarpK)
         return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
                                    a.key16 && a.m == 8 && a.nvals <= 0x8000, s);
@@ -293,6 +338,11 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
         rc = get_hk_big(device, d_pp, &h->hkb);
         if (rc) return rc;
         h->big_blocks = hs::big_blocks(h->sm_count, d_pp);
+        if (!hs::get_hk_two(device, d_pp, &h->two)) {
+            h->two_grid = hs::cluster_grid(h->two, h->sm_count);
+            h->stage_blocks = h->sm_count * 16;
+            h->two_chunk = 1024;
+        }
         for (int i = 0; i < 2; i++)
             CK(cudaMalloc(&h->big_scratch[i], (size_t)h->big_blocks * hs::hk_big_size(d_pp) * 8), "cudaMalloc scratch");
     } else {
@@ -316,6 +366,17 @@ int hs_instance_destroy(hs_instance* h) {
     if (h->rank16) cudaFree(h->rank16);
     for (int i = 0; i < 2; i++)
         if (h->big_scratch[i]) cudaFree(h->big_scratch[i]);
+    for (int i = 0; i < 2; i++) {
+        for (int j = 0; j < 2; j++) {
+            if (h->two_E[i][j]) cudaFree(h->two_E[i][j]);
+            if (h->two_dp[i][j]) cudaFree(h->two_dp[i][j]);
+            if (h->two_bad[i][j]) cudaFree(h->two_bad[i][j]);
+            if (h->two_ev_stage[i][j]) cudaEventDestroy(h->two_ev_stage[i][j]);
+            if (h->two_ev_hk[i][j]) cudaEventDestroy(h->two_ev_hk[i][j]);
+        }
+        if (h->two_side[i]) cudaStreamDestroy(h->two_side[i]);
+        if (h->two_ev_in[i]) cudaEventDestroy(h->two_ev_in[i]);
+    }
     if (h->heur_E) cudaFree(h->heur_E);
     cudaFree(h->invalid);
     for (int i = 0; i < 2; i++) {

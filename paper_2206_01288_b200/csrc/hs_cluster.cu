@@ -1,0 +1,365 @@
+// hs_cluster.cu -- exact pricing for 9 <= d_pp <= 16 without a stage order
+// (BASELINE configs 4 and 5: Held-Karp over up to 2^16 subsets).
+//
+// Two kernels per chunk of candidates:
+//   stage_kernel      one CTA per candidate (many per SM, latency hidden by
+//                     occupancy): validation, datap (numpy pairwise row
+//                     sums, group maxima) and the C(k,2) bottleneck edges of
+//                     the coarsened stage graph -> E in global memory.
+//   hk_cluster_kernel one thread-block cluster per candidate: Held-Karp
+//                     (combinatorics.py:258-276) keeping only popcount layers
+//                     p-1 and p, each layer split over the cluster's CTAs'
+//                     shared memory; a cluster barrier separates layers.
+//                     Tasks are "pushed": the CTA holding h[r][.] computes
+//                     every h[r | u][u] from local reads and stores the one
+//                     result into the owning CTA's slice (DSMEM store, no
+//                     remote-load latency on the critical path).  At k = 16
+//                     the two live layers are 2 x 102,960 doubles (1.65 MB):
+//                     8 CTAs x 206 KB, so the table never leaves the SMs.
+// Values are the reference's: h[s][u] = min_v (w[u][v] + h[s\u][v]) with
+// strict '<' (the min of a set of doubles does not depend on visit order),
+// total = first minimum over the full set.  Stage orders still use the
+// full-table CTA path (hs_big.cu).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "hs_cluster.h"
+#include "hs_cta_eval.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hs {
+
+constexpr int kClusterThreads = 512;
+static_assert(kStageES == kES16, "stage graph stride");
+
+template <typename KeyT, bool kM8>
+__global__ void __launch_bounds__(128) stage_kernel(EvalArgs a, double* __restrict__ Eout, double* __restrict__ dpout,
+                                                    uint8_t* __restrict__ bad_out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int k = a.k, m = kM8 ? 8 : a.m, km = k * m;
+    CtaScratch cs = cta_scratch_at(smem, k, m);
+    size_t off = cta_scratch_bytes(k, m);
+    int16_t* mem = reinterpret_cast<int16_t*>(smem + off);
+    off += ((size_t)km * 2 + 15) & ~(size_t)15;
+    uint32_t* seen = reinterpret_cast<uint32_t*>(smem + off);
+    __shared__ int bad;
+    const KeyT* RK = reinterpret_cast<const KeyT*>(a.rank);
+    const int nwords = (a.n + 31) >> 5;
+    for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
+        const int16_t* gsrc = a.groups + p * km;
+        for (int i = threadIdx.x; i < km; i += blockDim.x) mem[i] = gsrc[i];
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) seen[i] = 0;
+        if (threadIdx.x == 0) bad = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < km; i += blockDim.x) {  // costmodel.py:58-72
+            int d = mem[i];
+            if (d < 0 || d >= a.n || (i % m != 0 && mem[i - 1] >= d))
+                bad = 1;
+            else
+                atomicOr(&seen[d >> 5], 1u << (d & 31));
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
+            int bits = min(32, a.n - i * 32);
+            uint32_t want = bits == 32 ? 0xffffffffu : ((1u << bits) - 1u);
+            if (seen[i] != want) bad = 1;
+        }
+        __syncthreads();
+        if (bad) {
+            if (threadIdx.x == 0) {
+                const double nan = __longlong_as_double(0x7ff8000000000000LL);
+                if (a.datap) a.datap[p] = nan;
+                bad_out[p] = 1;
+                atomicAdd(a.invalid, 1);
+            }
+            __syncthreads();
+            continue;
+        }
+        const double datap = cta_stage<KeyT, kM8>(a.n, k, m, a.dp, RK, a.vals, cs, mem);
+        double* E = Eout + p * kStageStride;
+        for (int i = threadIdx.x; i < k * kES16; i += blockDim.x) E[i] = cs.E[i];
+        if (threadIdx.x == 0) {
+            dpout[p] = datap;
+            bad_out[p] = 0;
+            if (a.datap) a.datap[p] = datap;
+        }
+        if (a.per_group && threadIdx.x < k) a.per_group[p * k + threadIdx.x] = cs.pg[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ double two_relax(const double* Eu, const double* hr, uint32_t r) {
+    double best = kInf;
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        const int v = __ffs(r) - 1;
+        r &= r - 1;
+        const double c = Eu[v] + hr[i];
+        best = c < best ? c : best;
+    }
+    return best;
+}
+
+// h[r][.] runs past this CTA's slice into the next one (rare)
+__device__ __forceinline__ double two_relax_split(const double* Eu, const double* own, const double* next, int lr,
+                                                  int C, int nv, uint32_t r) {
+    double best = kInf;
+    for (int i = 0; i < nv; i++) {
+        const int v = __ffs(r) - 1;
+        r &= r - 1;
+        const int li = lr + i;
+        const double c = Eu[v] + (li < C ? own[li] : next[li - C]);
+        best = c < best ? c : best;
+    }
+    return best;
+}
+
+__global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const double* __restrict__ E, int es,
+                                                                     int64_t estride, int k, int64_t B, HKTwo t,
+                                                                     const double* __restrict__ add,
+                                                                     const uint8_t* __restrict__ bad,
+                                                                     double* __restrict__ out_total,
+                                                                     double* __restrict__ out_pipe) {
+    extern __shared__ __align__(16) double sm2[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(), cs = t.cs;
+    double* buf[2] = {sm2, sm2 + t.Cmax};
+    double* Es = sm2 + 2 * t.Cmax;
+    __shared__ double* rb[2][8];
+    if (threadIdx.x < cs) {
+        rb[0][threadIdx.x] = cl.map_shared_rank(buf[0], (int)threadIdx.x);
+        rb[1][threadIdx.x] = cl.map_shared_rank(buf[1], (int)threadIdx.x);
+    }
+    __syncthreads();
+    const int64_t ncl = gridDim.x / cs;
+    for (int64_t b = blockIdx.x / cs; b < B; b += ncl) {
+        const bool skip = bad && bad[b];  // same for every CTA of the cluster
+        if (!skip) {
+            const double* src = E + b * estride;
+            for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+                const int rr = i / k, cc = i - rr * k;
+                Es[rr * kES16 + cc] = src[(size_t)rr * es + cc];
+            }
+        }
+        __syncthreads();
+        cl.sync();  // every reader of the previous candidate is done
+        if (!skip) {
+            for (int p = 2; p <= k; p++) {
+                const double* own = buf[(p - 1) & 1];
+                const double* next = rank + 1 < cs ? rb[(p - 1) & 1][rank + 1] : own;
+                double* const* dst = rb[p & 1];
+                const int Cin = t.C[p - 1];
+                const int end = t.tbeg[p][rank + 1];
+                int x = t.tbeg[p][rank] + (int)threadIdx.x;
+                uint64_t wn = x < end ? __ldg(t.tasks + x) : 0;  // task words are prefetched one ahead
+                for (; x < end; x += blockDim.x) {
+                    const uint64_t w = wn;
+                    if (x + (int)blockDim.x < end) wn = __ldg(t.tasks + x + blockDim.x);
+                    const int u = (int)(w & 0xF);
+                    const uint32_t r = (uint32_t)(w >> 4) & 0xFFFFu;
+                    const double* Eu = Es + u * kES16;
+                    double best;
+                    if (p == 2) {
+                        best = Eu[__ffs(r) - 1];  // w[u][v] + 0.0
+                    } else {
+                        const int lr = (int)(w >> 20) & 0x1FFFF;
+                        if (w >> 63) {
+                            best = two_relax_split(Eu, own, next, lr, Cin, p - 1, r);
+                        } else {
+                            const double* hr = own + lr;
+                            switch (p) {
+                                case 3: best = two_relax<2>(Eu, hr, r); break;
+                                case 4: best = two_relax<3>(Eu, hr, r); break;
+                                case 5: best = two_relax<4>(Eu, hr, r); break;
+                                case 6: best = two_relax<5>(Eu, hr, r); break;
+                                case 7: best = two_relax<6>(Eu, hr, r); break;
+                                case 8: best = two_relax<7>(Eu, hr, r); break;
+                                case 9: best = two_relax<8>(Eu, hr, r); break;
+                                case 10: best = two_relax<9>(Eu, hr, r); break;
+                                case 11: best = two_relax<10>(Eu, hr, r); break;
+                                case 12: best = two_relax<11>(Eu, hr, r); break;
+                                case 13: best = two_relax<12>(Eu, hr, r); break;
+                                case 14: best = two_relax<13>(Eu, hr, r); break;
+                                case 15: best = two_relax<14>(Eu, hr, r); break;
+                                default: best = two_relax<15>(Eu, hr, r); break;
+                            }
+                        }
+                    }
+                    dst[(w >> 37) & 7][(w >> 40) & 0x1FFFF] = best;
+                }
+                cl.sync();
+            }
+            if (rank == 0 && threadIdx.x == 0) {  // layer k: the full set's k entries, slots 0..k-1
+                const int Ck = t.C[k];
+                double* const* fin = rb[k & 1];
+                double tot = fin[0][0];
+                for (int u = 1; u < k; u++) tot = dmin(tot, fin[u / Ck][u % Ck]);
+                if (add) {
+                    out_total[b] = add[b] + tot;
+                    if (out_pipe) out_pipe[b] = tot;
+                } else {
+                    out_total[b] = tot;
+                }
+            }
+        } else if (rank == 0 && threadIdx.x == 0) {
+            const double nan = __longlong_as_double(0x7ff8000000000000LL);
+            out_total[b] = nan;
+            if (out_pipe) out_pipe[b] = nan;
+        }
+    }
+    cl.sync();  // no CTA leaves while a peer may still touch its shared memory
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+namespace {
+struct DeviceHKTwo {
+    uint64_t* st = nullptr;
+    HKTwo t{};
+};
+std::mutex g_two_mu;
+std::map<std::pair<int, int>, DeviceHKTwo> g_two;
+
+uint64_t binom(int n, int r) {
+    if (r < 0 || r > n) return 0;
+    uint64_t v = 1;
+    for (int i = 1; i <= r; i++) v = v * (uint64_t)(n - r + i) / (uint64_t)i;
+    return v;
+}
+}  // namespace
+
+size_t cluster_smem_bytes(const HKTwo& t) { return (size_t)(2 * t.Cmax + 16 * kES16) * 8; }
+
+int get_hk_two(int device, int k, HKTwo* out) {
+    if (k < 2 || k > 16) return -3;
+    std::lock_guard<std::mutex> lk(g_two_mu);
+    auto key = std::make_pair(device, k);
+    auto it = g_two.find(key);
+    if (it == g_two.end()) {
+        int optin = 0;
+        if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) return -1;
+        uint64_t size[18] = {0};
+        for (int p = 1; p <= k; p++) size[p] = binom(k, p) * (uint64_t)p;
+        uint64_t maxS = 0;
+        for (int p = 2; p <= k; p++) maxS = std::max<uint64_t>(maxS, size[p]);
+        DeviceHKTwo d;
+        d.t.cs = 0;
+        for (int cs = 1; cs <= 8; cs *= 2) {
+            const uint64_t C = (maxS + cs - 1) / cs;
+            if ((2 * C + 16 * kES16) * 8 + 1024 <= (uint64_t)optin) {
+                d.t.cs = cs;
+                break;
+            }
+        }
+        if (!d.t.cs) return -3;
+        const int cs = d.t.cs;
+        d.t.Cmax = 0;
+        for (int p = 0; p < 18; p++) {
+            d.t.C[p] = p >= 1 && p <= k ? (int)((size[p] + cs - 1) / cs) : 1;
+            if (p >= 2 && p <= k) d.t.Cmax = std::max(d.t.Cmax, d.t.C[p]);
+        }
+        std::vector<int> rank_of((size_t)1 << k, 0), cnt(k + 2, 0);
+        for (int s = 0; s < (1 << k); s++) rank_of[s] = cnt[__builtin_popcount(s)]++;
+        std::vector<uint64_t> st;
+        st.reserve(((size_t)k << (k - 1)));
+        std::vector<std::vector<uint64_t>> per(cs);
+        for (int p = 0; p < 18; p++) {
+            for (int q = 0; q < 9; q++) d.t.tbeg[p][q] = (int)st.size();
+            if (p < 2 || p > k) continue;
+            for (auto& v : per) v.clear();
+            const uint64_t Cin = (uint64_t)d.t.C[p - 1], Cout = (uint64_t)d.t.C[p];
+            int spread = 0;
+            for (int r = 1; r < (1 << k); r++) {  // sources in slot order of layer p-1
+                if (__builtin_popcount(r) != p - 1) continue;
+                const uint64_t slot = (uint64_t)rank_of[r] * (uint64_t)(p - 1);
+                int owner;
+                uint64_t w0 = (uint64_t)r << 4;
+                if (p >= 3) {
+                    owner = (int)(slot / Cin);
+                    const uint64_t lr = slot % Cin;
+                    w0 |= (lr << 20) | ((lr + (uint64_t)(p - 1) > Cin) ? (1ull << 63) : 0ull);
+                } else {
+                    owner = spread++ % cs;  // layer 1 is implicit zeros: deal tasks round-robin
+                }
+                for (int u = 0; u < k; u++) {
+                    if (r >> u & 1) continue;
+                    const int s = r | (1 << u);
+                    const uint64_t dslot = (uint64_t)rank_of[s] * (uint64_t)p + __builtin_popcount(s & ((1 << u) - 1));
+                    per[owner].push_back(w0 | (uint64_t)u | ((dslot / Cout) << 37) | ((dslot % Cout) << 40));
+                }
+            }
+            for (int q = 0; q < cs; q++) {
+                d.t.tbeg[p][q] = (int)st.size();
+                st.insert(st.end(), per[q].begin(), per[q].end());
+            }
+            for (int q = cs; q < 9; q++) d.t.tbeg[p][q] = (int)st.size();
+        }
+        if (cudaMalloc(&d.st, st.size() * 8) != cudaSuccess) return -1;
+        if (cudaMemcpy(d.st, st.data(), st.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+        d.t.tasks = d.st;
+        it = g_two.emplace(key, d).first;
+    }
+    *out = it->second.t;
+    return 0;
+}
+
+int cluster_grid(const HKTwo& t, int sm_count) {
+    const size_t smem = cluster_smem_bytes(t) + 256;
+    int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (228u << 10) / smem));
+    if (t.cs > 1) per_sm = 1;
+    return std::max(1, sm_count / t.cs) * t.cs * per_sm;
+}
+
+template <typename KT, bool M8>
+static void launch_stage_t(const EvalArgs& a, double* E, double* dp, uint8_t* bad, int blocks, cudaStream_t s) {
+    size_t smem = cta_scratch_bytes(a.k, M8 ? 8 : a.m) + (((size_t)a.k * a.m * 2 + 15) & ~(size_t)15) + 32 * 4 * 4;
+    cudaFuncSetAttribute(stage_kernel<KT, M8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    stage_kernel<KT, M8><<<blocks, 128, smem, s>>>(a, E, dp, bad);
+}
+
+int launch_stage(const EvalArgs& a, double* E, double* datap, uint8_t* bad, int blocks, bool m8, cudaStream_t s) {
+    if (a.P == 0) return 0;
+    blocks = (int)std::min<int64_t>(blocks, a.P);
+    if (m8)
+        launch_stage_t<uint16_t, true>(a, E, datap, bad, blocks, s);
+    else if (a.key16)
+        launch_stage_t<uint16_t, false>(a, E, datap, bad, blocks, s);
+    else
+        launch_stage_t<uint32_t, false>(a, E, datap, bad, blocks, s);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+int launch_hk_cluster(const double* E, int es, int64_t estride, int k, int64_t B, const HKTwo& t, int grid,
+                      const double* add, const uint8_t* bad, double* out_total, double* out_pipe, cudaStream_t s) {
+    if (B == 0) return 0;
+    const int clusters = (int)std::min<int64_t>(grid / t.cs, B);
+    const size_t smem = cluster_smem_bytes(t);
+    if (cudaFuncSetAttribute(hk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+        return -1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(clusters * t.cs), 1, 1);
+    cfg.blockDim = dim3(kClusterThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)t.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, hk_cluster_kernel, E, es, estride, k, B, t, add, bad, out_total, out_pipe) !=
+        cudaSuccess)
+        return -1;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace hs

@@ -1,0 +1,50 @@
+// hs_cluster.h -- host interface of the cluster Held-Karp path (9 <= d_pp <= 16,
+// pricing without a stage order).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hs_internal.h"
+
+namespace hs {
+
+constexpr int kStageES = 17;                  // padded stage-graph row (= kES16)
+constexpr int kStageStride = 16 * kStageES;   // doubles per staged candidate
+
+// Two-layer Held-Karp schedule, "push" form.  Layer p holds the entries
+// h[s][u], |s| = p, u in s, at slot rank_p(s) * p + (rank of u in s), where
+// rank_p orders the p-subsets as integers; the slots are split into cs
+// balanced slices of C[p] = ceil(size_p / cs), slice q living in the shared
+// memory of CTA q of the cluster.  Layer p is produced by tasks (r, u),
+// |r| = p - 1, u not in r: h[r | u][u] = min_v (w[u][v] + h[r][v]).  A task
+// runs on the CTA that holds h[r][.] (local reads) and stores its one result
+// into the slice that owns slot (r | u, u) (a DSMEM store).  Task word:
+// u (4) | r (16) << 4 | local slot of h[r][first member] (17) << 20 |
+// destination CTA (3) << 37 | destination local slot (17) << 40 |
+// "h[r][.] runs into the next CTA's slice" (1) << 63.  Tasks of layer p for
+// CTA q are [tbeg[p][q], tbeg[p][q + 1]).
+struct HKTwo {
+    const uint64_t* tasks;
+    int tbeg[18][9];
+    int C[18];    // slice length per layer
+    int Cmax;     // buffer length (max over layers)
+    int cs;       // CTAs per cluster (1, 2, 4 or 8)
+};
+
+int get_hk_two(int device, int k, HKTwo* out);
+size_t cluster_smem_bytes(const HKTwo& t);
+// grid in CTAs for one pricing launch (a multiple of t.cs)
+int cluster_grid(const HKTwo& t, int sm_count);
+
+// Stage kernel: validation, datap / per_group and the padded stage graph
+// E[b] (16 x 17 doubles) of partitions [0, P) of a.groups; bad[b] = 1 for
+// malformed ones (their outputs are NaN, a.invalid counts them).
+int launch_stage(const EvalArgs& a, double* E, double* datap, uint8_t* bad, int blocks, bool m8, cudaStream_t s);
+
+// Held-Karp totals of B stage graphs: E + b * estride, row stride es; when
+// `add` is given, out_total[b] = add[b] + path and out_pipe[b] = path,
+// else out_total[b] = path; bad[b] (nullable) skips a graph (NaN outputs).
+int launch_hk_cluster(const double* E, int es, int64_t estride, int k, int64_t B, const HKTwo& t, int grid,
+                      const double* add, const uint8_t* bad, double* out_total, double* out_pipe, cudaStream_t s);
+
+}  // namespace hs

@@ -135,13 +135,12 @@ __device__ inline CtaScratch cta_scratch_at(unsigned char* base, int k, int m) {
     return c;
 }
 
-// All threads of the CTA price the partition in mem[k*m] (smem).  Returns
-// (datap, pipe) in every thread; cs.pg holds per_group_datap and h the
-// Held-Karp table (for order reconstruction).
+// All threads of the CTA stage the partition in mem[k*m] (smem): cs.pg gets
+// per_group_datap (costmodel.py:154-175), cs.E the coarsened stage graph
+// (bottleneck edges, costmodel.py:200-208, zero diagonal).  Returns datap.
 template <typename KeyT, bool kM8>
-__device__ inline void cta_price(int n, int k, int m_rt, const double* DP, const KeyT* RK, const double* vals,
-                                 const HKBig& t, const CtaScratch& cs, double* h, const int16_t* mem, double& datap,
-                                 double& pipe) {
+__device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, const KeyT* RK, const double* vals,
+                                   const CtaScratch& cs, const int16_t* mem) {
     const int m = kM8 ? 8 : m_rt, km = k * m;
     for (int r = threadIdx.x; r < km; r += blockDim.x) {
         int g = r / m;
@@ -181,10 +180,20 @@ __device__ inline void cta_price(int n, int k, int m_rt, const double* DP, const
     }
     if (threadIdx.x < k) cs.E[threadIdx.x * kES16 + threadIdx.x] = 0.0;
     __syncthreads();
-    pipe = cta_held_karp(k, cs.E, h, t, cs.red);
     double dp = cs.pg[0];
     for (int g = 1; g < k; g++) dp = dmax(dp, cs.pg[g]);
-    datap = dp;
+    return dp;
+}
+
+// All threads of the CTA price the partition in mem[k*m] (smem).  Returns
+// (datap, pipe) in every thread; cs.pg holds per_group_datap and h the
+// Held-Karp table (for order reconstruction).
+template <typename KeyT, bool kM8>
+__device__ inline void cta_price(int n, int k, int m_rt, const double* DP, const KeyT* RK, const double* vals,
+                                 const HKBig& t, const CtaScratch& cs, double* h, const int16_t* mem, double& datap,
+                                 double& pipe) {
+    datap = cta_stage<KeyT, kM8>(n, k, m_rt, DP, RK, vals, cs, mem);
+    pipe = cta_held_karp(k, cs.E, h, t, cs.red);
 }
 
 

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "../../include/hetsched_b200.h"
+#include "hs_cluster.h"
 #include "hs_internal.h"
 
 namespace hsx {
@@ -46,6 +47,15 @@ struct hs_instance {
     hs::HKBig hkb{};               // d_pp > 8: CTA evaluator schedule
     double* big_scratch[2] = {nullptr, nullptr};  // per-CTA Held-Karp slices (two stream sets)
     int big_blocks = 0;
+    // d_pp 9..16 without stage order: stage kernel + cluster Held-Karp (hs_cluster.cu)
+    hs::HKTwo two{};
+    int two_grid = 0, stage_blocks = 0;
+    int64_t two_chunk = 0;
+    double* two_E[2][2] = {};     // [stream set][ping-pong]
+    double* two_dp[2][2] = {};
+    uint8_t* two_bad[2][2] = {};
+    cudaStream_t two_side[2] = {};
+    cudaEvent_t two_ev_stage[2][2] = {}, two_ev_hk[2][2] = {}, two_ev_in[2] = {};
     double* heur_E = nullptr;      // d_pp > 16: per-CTA stage graphs for the heuristic path
     int* invalid = nullptr;
     hs::EvalPlan plan{};

@@ -241,3 +241,44 @@ def test_no_order_evaluator_invalid_ragged_and_offset_views():
     good[[0, 31, 32, 500, 999]] = False
     assert np.isnan(got[~good]).all()
     assert np.array_equal(got[good], ref[good])
+
+
+@pytest.mark.parametrize("name,count", [("r32_16x2", 300), ("r48_12x4", 200), ("r128_16x8", 100), ("config4", 40),
+                                        ("r18_9x2", 300)])
+def test_cluster_held_karp_no_order_vs_oracle(name, count):
+    """order=False at d_pp 9..16: stage kernel + cluster Held-Karp (two live
+    layers in distributed shared memory) vs the oracle, bit for bit."""
+    g, w = I.instance(name)
+    parts = _random_parts(37, count, g.n, w.d_pp, w.d_dp)
+    r = hs.comm_cost_batch(g, parts, w, per_group=True)
+    t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"], t) and np.array_equal(r["datap"], d) and np.array_equal(r["pipelinep"], p)
+    full = hs.comm_cost_batch(g, parts[:8], w, per_group=True, order=True)
+    assert np.array_equal(r["per_group"][:8], full["per_group"])
+
+
+@pytest.mark.parametrize("k", [9, 12, 13, 14, 15, 16])
+def test_cluster_held_karp_every_cluster_size(k):
+    """k = 9..13 fit one CTA, 14 / 15 / 16 split the live layers over 2 / 4 / 8."""
+    from paper_2206_01288_b200.netmodel import random_graph
+    from paper_2206_01288_b200.workload import WorkloadSpec
+    g = random_graph(100 + k, 3 * k)
+    w = WorkloadSpec(k, 3, 1 << 30, 3 << 26)
+    parts = _random_parts(k, 64, g.n, k, 3)
+    r = hs.comm_cost_batch(g, parts, w)
+    t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"], t) and np.array_equal(r["pipelinep"], p)
+
+
+def test_cluster_held_karp_device_batch_with_malformed_rows():
+    """Device-tensor input: malformed rows are counted and raise, like the CTA path."""
+    import torch
+    g, w = I.instance("config4")
+    parts = _random_parts(41, 20, g.n, w.d_pp, w.d_dp)
+    bad = parts.copy()
+    bad[3, 0, 0], bad[3, 0, 1] = bad[3, 0, 1], bad[3, 0, 0]  # not ascending
+    with pytest.raises(hs.CostModelError):
+        hs.comm_cost_batch(g, torch.from_numpy(bad).cuda(), w)
+    r = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w)
+    t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+    assert np.array_equal(r["total"].cpu().numpy(), t)
