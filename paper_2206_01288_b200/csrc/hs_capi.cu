@@ -482,7 +482,12 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     for (int64_t c = 0; lo < P; c++) {
         int b = (int)(c & 1);
         cudaStream_t s = h->cs[b];
-        int64_t cnt = std::min<int64_t>(c == 0 ? h->chunk / 8 : h->chunk, P - lo);
+        // ramp: a small first chunk (short exposed H2D) and a small last one
+        // (short exposed D2H); full chunks in between
+        const int64_t small = h->chunk / 8, left = P - lo;
+        int64_t cnt = c == 0 ? small : h->chunk;
+        if (c > 0 && left > small && left <= h->chunk + small) cnt = left - small;
+        cnt = std::min<int64_t>(cnt, left);
         CK(cudaMemcpyAsync(h->cg[b], groups + lo * km, (size_t)cnt * km * 2, cudaMemcpyHostToDevice, s), "H2D");
         a.groups = h->cg[b];
         a.P = cnt;
