@@ -268,7 +268,7 @@ static int launch_two(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream
 
 static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
     if (h->k > 16) return hsx::fail(-3, "exact pricing is limited to d_pp <= 16 (Held-Karp); use heuristic paths");
-    if (h->k > hs::kWarpK && !a.order && h->two.tasks) return launch_two(h, a, set, s);
+    if (h->k > hs::kWarpK && !a.order && h->two.rwords) return launch_two(h, a, set, s);
     if (h->k > hs::kWarpK)
         return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
                                    a.key16 && a.m == 8 && a.nvals <= 0x8000, s);

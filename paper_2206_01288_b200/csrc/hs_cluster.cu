@@ -93,31 +93,57 @@ __global__ void __launch_bounds__(128) stage_kernel(EvalArgs a, double* __restri
     }
 }
 
+// One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
+// w[.][v] for v in r stay in registers while every u not in r is relaxed.
 template <int NV>
-__device__ __forceinline__ double two_relax(const double* Eu, const double* hr, uint32_t r) {
-    double best = kInf;
+__device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
+                                           uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
+                                           double* const* dst) {
+    uint32_t r = (uint32_t)(rw & 0xFFFF);
+    const int lr = (int)(rw >> 16) & 0x1FFFF;
+    const bool straddle = (rw >> 33) & 1;
+    const uint32_t* dw = dwords + (rw >> 34);
+    double hv[NV];
+    uint32_t voff[NV];
 #pragma unroll
     for (int i = 0; i < NV; i++) {
         const int v = __ffs(r) - 1;
         r &= r - 1;
-        const double c = Eu[v] + hr[i];
-        best = c < best ? c : best;
+        voff[i] = (uint32_t)v * 8u;
+        const int li = lr + i;
+        hv[i] = (!straddle || li < Cin) ? own[li] : next[li - Cin];
     }
-    return best;
+    uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
+    uint32_t dn = __ldg(dw);
+    for (int j = 0; rest; j++) {
+        const int u = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const uint32_t d = dn;
+        if (rest) dn = __ldg(dw + j + 1);
+        const char* Eu = reinterpret_cast<const char*>(Es + u * kES16);
+        double best = kInf;
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            const double c = *reinterpret_cast<const double*>(Eu + voff[i]) + hv[i];
+            best = c < best ? c : best;
+        }
+        dst[d >> 17][d & 0x1FFFF] = best;
+    }
 }
 
-// h[r][.] runs past this CTA's slice into the next one (rare)
-__device__ __forceinline__ double two_relax_split(const double* Eu, const double* own, const double* next, int lr,
-                                                  int C, int nv, uint32_t r) {
-    double best = kInf;
-    for (int i = 0; i < nv; i++) {
-        const int v = __ffs(r) - 1;
-        r &= r - 1;
-        const int li = lr + i;
-        const double c = Eu[v] + (li < C ? own[li] : next[li - C]);
-        best = c < best ? c : best;
+// layer 2: r = {v}, h[r][v] = 0 (implicit): h[{u, v}][u] = w[u][v]
+__device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, uint32_t full,
+                                                 const uint32_t* __restrict__ dwords, double* const* dst) {
+    const uint32_t r = (uint32_t)(rw & 0xFFFF);
+    const int v = __ffs(r) - 1;
+    const uint32_t* dw = dwords + (rw >> 34);
+    uint32_t rest = full & ~r;
+    for (int j = 0; rest; j++) {
+        const int u = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const uint32_t d = __ldg(dw + j);
+        dst[d >> 17][d & 0x1FFFF] = Es[u * kES16 + v];  // w[u][v] + 0.0
     }
-    return best;
 }
 
 __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const double* __restrict__ E, int es,
@@ -150,48 +176,32 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
         __syncthreads();
         cl.sync();  // every reader of the previous candidate is done
         if (!skip) {
+            const uint32_t full = (1u << k) - 1u;
             for (int p = 2; p <= k; p++) {
                 const double* own = buf[(p - 1) & 1];
                 const double* next = rank + 1 < cs ? rb[(p - 1) & 1][rank + 1] : own;
                 double* const* dst = rb[p & 1];
                 const int Cin = t.C[p - 1];
-                const int end = t.tbeg[p][rank + 1];
-                int x = t.tbeg[p][rank] + (int)threadIdx.x;
-                uint64_t wn = x < end ? __ldg(t.tasks + x) : 0;  // task words are prefetched one ahead
-                for (; x < end; x += blockDim.x) {
-                    const uint64_t w = wn;
-                    if (x + (int)blockDim.x < end) wn = __ldg(t.tasks + x + blockDim.x);
-                    const int u = (int)(w & 0xF);
-                    const uint32_t r = (uint32_t)(w >> 4) & 0xFFFFu;
-                    const double* Eu = Es + u * kES16;
-                    double best;
-                    if (p == 2) {
-                        best = Eu[__ffs(r) - 1];  // w[u][v] + 0.0
-                    } else {
-                        const int lr = (int)(w >> 20) & 0x1FFFF;
-                        if (w >> 63) {
-                            best = two_relax_split(Eu, own, next, lr, Cin, p - 1, r);
-                        } else {
-                            const double* hr = own + lr;
-                            switch (p) {
-                                case 3: best = two_relax<2>(Eu, hr, r); break;
-                                case 4: best = two_relax<3>(Eu, hr, r); break;
-                                case 5: best = two_relax<4>(Eu, hr, r); break;
-                                case 6: best = two_relax<5>(Eu, hr, r); break;
-                                case 7: best = two_relax<6>(Eu, hr, r); break;
-                                case 8: best = two_relax<7>(Eu, hr, r); break;
-                                case 9: best = two_relax<8>(Eu, hr, r); break;
-                                case 10: best = two_relax<9>(Eu, hr, r); break;
-                                case 11: best = two_relax<10>(Eu, hr, r); break;
-                                case 12: best = two_relax<11>(Eu, hr, r); break;
-                                case 13: best = two_relax<12>(Eu, hr, r); break;
-                                case 14: best = two_relax<13>(Eu, hr, r); break;
-                                case 15: best = two_relax<14>(Eu, hr, r); break;
-                                default: best = two_relax<15>(Eu, hr, r); break;
-                            }
-                        }
+                const int end = t.rbeg[p][rank + 1];
+                for (int x = t.rbeg[p][rank] + (int)threadIdx.x; x < end; x += blockDim.x) {
+                    const uint64_t rw = __ldg(t.rwords + x);
+                    switch (p) {
+                        case 2: two_source_first(Es, rw, full, t.dwords, dst); break;
+                        case 3: two_source<2>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 4: two_source<3>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 5: two_source<4>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 6: two_source<5>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 7: two_source<6>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 8: two_source<7>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 9: two_source<8>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 10: two_source<9>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 11: two_source<10>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 12: two_source<11>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 13: two_source<12>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 14: two_source<13>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        case 15: two_source<14>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
+                        default: two_source<15>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
                     }
-                    dst[(w >> 37) & 7][(w >> 40) & 0x1FFFF] = best;
                 }
                 cl.sync();
             }
@@ -221,7 +231,8 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
 
 namespace {
 struct DeviceHKTwo {
-    uint64_t* st = nullptr;
+    uint64_t* rw = nullptr;
+    uint32_t* dw = nullptr;
     HKTwo t{};
 };
 std::mutex g_two_mu;
@@ -267,43 +278,55 @@ int get_hk_two(int device, int k, HKTwo* out) {
         }
         std::vector<int> rank_of((size_t)1 << k, 0), cnt(k + 2, 0);
         for (int s = 0; s < (1 << k); s++) rank_of[s] = cnt[__builtin_popcount(s)]++;
-        std::vector<uint64_t> st;
-        st.reserve(((size_t)k << (k - 1)));
+        std::vector<uint64_t> rws;
+        std::vector<uint32_t> dws;
+        dws.reserve(((size_t)k << (k - 1)));
         std::vector<std::vector<uint64_t>> per(cs);
+        std::vector<std::vector<uint32_t>> perd(cs);
         for (int p = 0; p < 18; p++) {
-            for (int q = 0; q < 9; q++) d.t.tbeg[p][q] = (int)st.size();
+            for (int q = 0; q < 9; q++) d.t.rbeg[p][q] = (int)rws.size();
             if (p < 2 || p > k) continue;
-            for (auto& v : per) v.clear();
+            for (int q = 0; q < cs; q++) {
+                per[q].clear();
+                perd[q].clear();
+            }
             const uint64_t Cin = (uint64_t)d.t.C[p - 1], Cout = (uint64_t)d.t.C[p];
             int spread = 0;
             for (int r = 1; r < (1 << k); r++) {  // sources in slot order of layer p-1
                 if (__builtin_popcount(r) != p - 1) continue;
-                const uint64_t slot = (uint64_t)rank_of[r] * (uint64_t)(p - 1);
+                uint64_t w = (uint64_t)r;
                 int owner;
-                uint64_t w0 = (uint64_t)r << 4;
                 if (p >= 3) {
+                    const uint64_t slot = (uint64_t)rank_of[r] * (uint64_t)(p - 1);
                     owner = (int)(slot / Cin);
                     const uint64_t lr = slot % Cin;
-                    w0 |= (lr << 20) | ((lr + (uint64_t)(p - 1) > Cin) ? (1ull << 63) : 0ull);
+                    w |= (lr << 16) | ((lr + (uint64_t)(p - 1) > Cin) ? (1ull << 33) : 0ull);
                 } else {
-                    owner = spread++ % cs;  // layer 1 is implicit zeros: deal tasks round-robin
+                    owner = spread++ % cs;  // layer 1 is implicit zeros: deal sources round-robin
                 }
+                w |= (uint64_t)perd[owner].size() << 34;  // relative; rebased below
+                per[owner].push_back(w);
                 for (int u = 0; u < k; u++) {
                     if (r >> u & 1) continue;
                     const int s = r | (1 << u);
-                    const uint64_t dslot = (uint64_t)rank_of[s] * (uint64_t)p + __builtin_popcount(s & ((1 << u) - 1));
-                    per[owner].push_back(w0 | (uint64_t)u | ((dslot / Cout) << 37) | ((dslot % Cout) << 40));
+                    const uint64_t ds = (uint64_t)rank_of[s] * (uint64_t)p + __builtin_popcount(s & ((1 << u) - 1));
+                    perd[owner].push_back((uint32_t)(((ds / Cout) << 17) | (ds % Cout)));
                 }
             }
             for (int q = 0; q < cs; q++) {
-                d.t.tbeg[p][q] = (int)st.size();
-                st.insert(st.end(), per[q].begin(), per[q].end());
+                d.t.rbeg[p][q] = (int)rws.size();
+                const uint64_t base = dws.size();
+                for (uint64_t w : per[q]) rws.push_back(w + (base << 34));
+                dws.insert(dws.end(), perd[q].begin(), perd[q].end());
             }
-            for (int q = cs; q < 9; q++) d.t.tbeg[p][q] = (int)st.size();
+            for (int q = cs; q < 9; q++) d.t.rbeg[p][q] = (int)rws.size();
         }
-        if (cudaMalloc(&d.st, st.size() * 8) != cudaSuccess) return -1;
-        if (cudaMemcpy(d.st, st.data(), st.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
-        d.t.tasks = d.st;
+        if (cudaMalloc(&d.rw, rws.size() * 8) != cudaSuccess) return -1;
+        if (cudaMalloc(&d.dw, dws.size() * 4) != cudaSuccess) return -1;
+        if (cudaMemcpy(d.rw, rws.data(), rws.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+        if (cudaMemcpy(d.dw, dws.data(), dws.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+        d.t.rwords = d.rw;
+        d.t.dwords = d.dw;
         it = g_two.emplace(key, d).first;
     }
     *out = it->second.t;

@@ -15,17 +15,20 @@ constexpr int kStageStride = 16 * kStageES;   // doubles per staged candidate
 // h[s][u], |s| = p, u in s, at slot rank_p(s) * p + (rank of u in s), where
 // rank_p orders the p-subsets as integers; the slots are split into cs
 // balanced slices of C[p] = ceil(size_p / cs), slice q living in the shared
-// memory of CTA q of the cluster.  Layer p is produced by tasks (r, u),
-// |r| = p - 1, u not in r: h[r | u][u] = min_v (w[u][v] + h[r][v]).  A task
-// runs on the CTA that holds h[r][.] (local reads) and stores its one result
-// into the slice that owns slot (r | u, u) (a DSMEM store).  Task word:
-// u (4) | r (16) << 4 | local slot of h[r][first member] (17) << 20 |
-// destination CTA (3) << 37 | destination local slot (17) << 40 |
-// "h[r][.] runs into the next CTA's slice" (1) << 63.  Tasks of layer p for
-// CTA q are [tbeg[p][q], tbeg[p][q + 1]).
+// memory of CTA q of the cluster.  Layer p is produced r-major: the CTA that
+// holds h[r][.] (|r| = p - 1) loads those p - 1 values once and computes
+// h[r | u][u] = min_v (w[u][v] + h[r][v]) for every u not in r, storing each
+// result into the slice that owns slot (r | u, u) (a DSMEM store).
+//   rwords[i]: r (16) | local slot of h[r][first member] (17) << 16 |
+//              "h[r][.] runs into the next CTA's slice" (1) << 33 |
+//              index of r's first destination word (30) << 34
+//   dwords[j]: destination CTA (3) << 17 | local slot (17), one per u not in
+//              r, ascending u
+// The sources of layer p on CTA q are rwords[rbeg[p][q] .. rbeg[p][q + 1]).
 struct HKTwo {
-    const uint64_t* tasks;
-    int tbeg[18][9];
+    const uint64_t* rwords;
+    const uint32_t* dwords;
+    int rbeg[18][9];
     int C[18];    // slice length per layer
     int Cmax;     // buffer length (max over layers)
     int cs;       // CTAs per cluster (1, 2, 4 or 8)
