@@ -67,6 +67,7 @@ __device__ inline double pw_array(const double* a, int n) {
 struct LS {
     int n, k, m, cap;
     const double* W;  // surrogate weights n x n (scheduler.py:84-88)
+    uint32_t w_sh;    // shared-window address of W when it was staged in shared memory, else 0
     int16_t* G;       // k x cap members, ascending
     int* sz;          // k sizes
     double* mean;     // n x k: mean[u*k+i] = seq_sum(W[u, G_i]) / sz_i, computed lazily
@@ -336,6 +337,31 @@ __device__ __forceinline__ void invalidate(LS& s, int j) {
 // sums of _gain_ours, and the swap is two byte-shifts of the packed words.
 // No shared-memory state changes until the pair settles.
 
+// W on the register driver paths: explicit ld.shared when the table was
+// staged in shared memory (through LS the compiler only sees a generic
+// pointer and would emit generic loads).  row(u) is a row handle (byte
+// address or element offset), at(row, v) reads w[u][v].
+template <bool kSh>
+struct WTab {
+    const double* g;
+    uint32_t sh, rowlen;
+    __device__ __forceinline__ uint32_t row(uint32_t u) const { return kSh ? sh + u * rowlen * 8u : u * rowlen; }
+    __device__ __forceinline__ double at(uint32_t r, uint32_t v) const {
+        if constexpr (kSh) {
+            double x;
+            asm("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(r + v * 8u));
+            return x;
+        } else {
+            return g[r + v];
+        }
+    }
+};
+
+template <bool kSh>
+__device__ __forceinline__ WTab<kSh> wtab(const LS& s) {
+    return WTab<kSh>{s.W, s.w_sh, (uint32_t)s.n};
+}
+
 __device__ __forceinline__ uint32_t byte_of(uint64_t x, uint32_t i) {
     return __byte_perm((uint32_t)x, (uint32_t)(x >> 32), i) & 0xFFu;
 }
@@ -366,12 +392,13 @@ __device__ __forceinline__ uint64_t ord_bits(double v) {
 }
 
 // _fast_edge of two packed groups at once; returns codes i*8+l (i < l)
-__device__ __forceinline__ void fast_edges8(const double* W, int n, uint64_t X, uint64_t Y, int lane, uint32_t pi,
+template <bool kSh>
+__device__ __forceinline__ void fast_edges8(const WTab<kSh>& W, uint64_t X, uint64_t Y, int lane, uint32_t pi,
                                             uint32_t pl, uint32_t& cx, uint32_t& cy) {
     uint64_t kx = ~0ull, ky = ~0ull;
     if (lane < 28) {
-        kx = ord_bits(W[byte_of(X, pi) * n + byte_of(X, pl)]);
-        ky = ord_bits(W[byte_of(Y, pi) * n + byte_of(Y, pl)]);
+        kx = ord_bits(W.at(W.row(byte_of(X, pi)), byte_of(X, pl)));
+        ky = ord_bits(W.at(W.row(byte_of(Y, pi)), byte_of(Y, pl)));
     }
     const uint32_t hx = (uint32_t)(kx >> 32), hy = (uint32_t)(ky >> 32);
     const uint32_t mhx = __reduce_min_sync(kFull, hx), mhy = __reduce_min_sync(kFull, hy);
@@ -384,9 +411,9 @@ __device__ __forceinline__ void fast_edges8(const double* W, int n, uint64_t X, 
 
 // the `for _ in range(d_dp)` loop of _pass_ours for pair (j, j2); true if a
 // swap was applied
+template <bool kSh>
 static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, uint32_t pl) {
-    const int n = s.n;
-    const double* W = s.W;
+    const WTab<kSh> W = wtab<kSh>(s);
     const int16_t* gj = s.G + j * s.cap;
     const int16_t* gj2 = s.G + j2 * s.cap;
     uint64_t X = 0, Y = 0;
@@ -399,19 +426,19 @@ static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, 
     bool changed = false;
     for (int it = 0; it < 8; it++) {
         uint32_t cx, cy;
-        fast_edges8(W, n, X, Y, lane, pi, pl, cx, cy);
+        fast_edges8<kSh>(W, X, Y, lane, pi, pl, cx, cy);
         const uint32_t d1 = byte_of(X, cx >> 3), d2 = byte_of(X, cx & 7);
         const uint32_t d1p = byte_of(Y, cy >> 3), d2p = byte_of(Y, cy & 7);
         // lane q: t_q = psum(w[u, other]) / 8 - w[u, partner]  (_gain_ours)
         const uint32_t u = q == 0 ? d1 : q == 1 ? d2 : q == 2 ? d1p : d2p;
         const uint32_t pu = q == 0 ? d2 : q == 1 ? d1 : q == 2 ? d2p : d1p;
         const uint64_t O = q < 2 ? Y : X;
-        const double* wr = W + (size_t)u * n;
+        const uint32_t wr = W.row(u);
         double r[8];
 #pragma unroll
-        for (int e = 0; e < 8; e++) r[e] = wr[byte_of(O, e)];
+        for (int e = 0; e < 8; e++) r[e] = W.at(wr, byte_of(O, e));
         const double sum = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        const double t = div_count(sum, 8) - wr[pu];
+        const double t = div_count(sum, 8) - W.at(wr, pu);
         const double t1a = __shfl_sync(kFull, t, 0), t1b = __shfl_sync(kFull, t, 1);
         const double t2a = __shfl_sync(kFull, t, 2), t2b = __shfl_sync(kFull, t, 3);
         // _best_candidate: (d1,d1p), (d1,d2p), (d2,d1p), (d2,d2p), first best
@@ -477,7 +504,8 @@ static __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
         int j, j2;
         decode_pair(s.perm[q], k, j, j2);
         if (fast8 && s.sz[j] == 8 && s.sz[j2] == 8) {
-            if (sweep_pair8(s, j, j2, lane, pi, pl)) changed = true;
+            if (s.w_sh ? sweep_pair8<true>(s, j, j2, lane, pi, pl) : sweep_pair8<false>(s, j, j2, lane, pi, pl))
+                changed = true;
             continue;
         }
         for (int it = 0; it < d_dp; it++) {
@@ -756,11 +784,11 @@ __device__ __forceinline__ void members_insert(Members& L, int c, uint32_t v) {
 
 // w[u, grp].mean() over cnt packed members: sequential sum (as numpy reduces
 // the F-contiguous gather), then / count; all loads issued up front
-template <int MAXC>
-__device__ __forceinline__ double members_mean(const double* wr, const Members& L, int cnt) {
+template <int MAXC, bool kSh>
+__device__ __forceinline__ double members_mean(const WTab<kSh>& W, uint32_t wr, const Members& L, int cnt) {
     double w[MAXC];
 #pragma unroll
-    for (int t = 0; t < MAXC; t++) w[t] = t < cnt ? wr[mbyte(L, t)] : 0.0;
+    for (int t = 0; t < MAXC; t++) w[t] = t < cnt ? W.at(wr, mbyte(L, t)) : 0.0;
     double r = 0.0;
 #pragma unroll
     for (int t = 0; t < MAXC; t++)
@@ -769,13 +797,14 @@ __device__ __forceinline__ double members_mean(const double* wr, const Members& 
 }
 
 // min of wr over the members other than `self` (order-free), +inf if none
-template <int MAXC>
-__device__ __forceinline__ double members_min(const double* wr, const Members& L, int cnt, uint32_t self) {
+template <int MAXC, bool kSh>
+__device__ __forceinline__ double members_min(const WTab<kSh>& W, uint32_t wr, const Members& L, int cnt,
+                                              uint32_t self) {
     double h = kInf;
 #pragma unroll
     for (int t = 0; t < MAXC; t++) {
         const uint32_t x = mbyte(L, t);
-        if (t < cnt && x != self) h = dmin(h, wr[x]);
+        if (t < cnt && x != self) h = dmin(h, W.at(wr, x));
     }
     return h;
 }
@@ -792,7 +821,8 @@ struct ChainRegs {
 // _move (:294-296): v leaves src for dst (bisect.insort keeps the order).
 // Home costs follow exactly (min is order-free): a member of dst takes
 // min(home, w[d, v]); a member of src keeps its home unless v was at it.
-__device__ __forceinline__ void cmove(const LS& s, ChainRegs& c, int v, int src, int dst, int lane) {
+template <bool kSh>
+__device__ __forceinline__ void cmove(const WTab<kSh>& W, ChainRegs& c, int v, int src, int dst, int lane) {
     const uint64_t bit = 1ull << v;
     if (lane == src) {
         members_remove(c.L, __popcll(c.GM & (bit - 1ull)));
@@ -807,7 +837,7 @@ __device__ __forceinline__ void cmove(const LS& s, ChainRegs& c, int v, int src,
         c.g0 = dst;
         c.st0 = true;
     } else if ((c.g0 == src || c.g0 == dst) && !(c.locked >> d0 & 1ull) && !c.st0) {
-        const double w = s.W[(size_t)d0 * s.n + v];
+        const double w = W.at(W.row((uint32_t)d0), (uint32_t)v);
         if (c.g0 == dst)
             c.h0 = dmin(c.h0, w);
         else if (!(w > c.h0))
@@ -817,7 +847,7 @@ __device__ __forceinline__ void cmove(const LS& s, ChainRegs& c, int v, int src,
         c.g1 = dst;
         c.st1 = true;
     } else if ((c.g1 == src || c.g1 == dst) && !(c.locked >> d1 & 1ull) && !c.st1) {
-        const double w = s.W[(size_t)d1 * s.n + v];
+        const double w = W.at(W.row((uint32_t)d1), (uint32_t)v);
         if (c.g1 == dst)
             c.h1 = dmin(c.h1, w);
         else if (!(w > c.h1))
@@ -826,21 +856,20 @@ __device__ __forceinline__ void cmove(const LS& s, ChainRegs& c, int v, int src,
 }
 
 // _home_costs (:287-291) for this lane's unlocked devices with a stale home
-template <int MAXC>
-__device__ __forceinline__ void refresh_homes(const LS& s, ChainRegs& c, int lane) {
+template <int MAXC, bool kSh>
+__device__ __forceinline__ void refresh_homes(const WTab<kSh>& W, ChainRegs& c, int lane) {
     const bool r0 = c.st0 && c.g0 >= 0 && !(c.locked >> lane & 1ull);
     const bool r1 = c.st1 && c.g1 >= 0 && !(c.locked >> (lane + 32) & 1ull);
     if (!__any_sync(kFull, r0 || r1)) return;
     const int s0 = c.g0 < 0 ? 0 : c.g0, s1 = c.g1 < 0 ? 0 : c.g1;
     const Members m0 = shfl_members(c.L, s0), m1 = shfl_members(c.L, s1);
     const int n0 = __popcll(shfl64(c.GM, s0)), n1 = __popcll(shfl64(c.GM, s1));
-    const int n = s.n;
     if (r0) {
-        c.h0 = members_min<MAXC>(s.W + (size_t)lane * n, m0, n0, (uint32_t)lane);
+        c.h0 = members_min<MAXC, kSh>(W, W.row((uint32_t)lane), m0, n0, (uint32_t)lane);
         c.st0 = false;
     }
     if (r1) {
-        c.h1 = members_min<MAXC>(s.W + (size_t)(lane + 32) * n, m1, n1, (uint32_t)(lane + 32));
+        c.h1 = members_min<MAXC, kSh>(W, W.row((uint32_t)(lane + 32)), m1, n1, (uint32_t)(lane + 32));
         c.st1 = false;
     }
 }
@@ -864,10 +893,11 @@ __device__ __forceinline__ int chain_fastest_free(const ChainRegs& c, int i, int
     return (cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
 }
 
-template <int MAXC>
+template <int MAXC, bool kSh>
 static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
-    const int k = s.k, n = s.n;
-    refresh_homes<MAXC>(s, c, lane);
+    const int k = s.k;
+    const WTab<kSh> W = wtab<kSh>(s);
+    refresh_homes<MAXC, kSh>(W, c, lane);
     // fastest_free of every group at once: three REDUX stages, 8 groups wide
     int vv[8];
     double hh[8];
@@ -914,7 +944,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
                 hi = hh[q];
             }
         double x = -kInf;
-        if (j < k && j != i && vi >= 0) x = members_mean<MAXC>(s.W + (size_t)vi * n, Lj, cj);
+        if (j < k && j != i && vi >= 0) x = members_mean<MAXC, kSh>(W, W.row((uint32_t)vi), Lj, cj);
         x = dmax(x, __shfl_xor_sync(kFull, x, 1));
         x = dmax(x, __shfl_xor_sync(kFull, x, 2));
         x = dmax(x, __shfl_xor_sync(kFull, x, 4));
@@ -936,13 +966,13 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     int cur = start, nm = 0;
     bool natural = false;
     for (int it = 0; it < k; it++) {
-        refresh_homes<MAXC>(s, c, lane);
+        refresh_homes<MAXC, kSh>(W, c, lane);
         double home;
         const int v = chain_fastest_free(c, cur, lane, home);
         if (v < 0) break;
         // scores = mean[v, targets]; dst = first maximum
         double mj = 0.0;
-        if (lane < k) mj = members_mean<MAXC>(s.W + (size_t)v * n, c.L, __popcll(c.GM));
+        if (lane < k) mj = members_mean<MAXC, kSh>(W, W.row((uint32_t)v), c.L, __popcll(c.GM));
         double sc;
         const int dst = redux_argmax(mj, lane < k && lane != cur, lane, sc);
         const double mstart = __shfl_sync(kFull, mj, start);
@@ -954,7 +984,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
             mv_dst[nm] = dst;
         }
         c.locked |= 1ull << v;
-        cmove(s, c, v, cur, dst, lane);
+        cmove<kSh>(W, c, v, cur, dst, lane);
         nm++;
         cur = dst;
         if (cur == start) {
@@ -979,13 +1009,13 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     }
     const bool applied = best_v > 0.0;
     const int keep = applied ? best_l : 0;
-    for (int t = nm - 1; t >= keep; t--) cmove(s, c, mv_v[t], mv_dst[t], mv_src[t], lane);
-    if (applied && best_l < nm) cmove(s, c, mv_v[best_l], mv_src[best_l], start, lane);
+    for (int t = nm - 1; t >= keep; t--) cmove<kSh>(W, c, mv_v[t], mv_dst[t], mv_src[t], lane);
+    if (applied && best_l < nm) cmove<kSh>(W, c, mv_v[best_l], mv_src[best_l], start, lane);
     __syncwarp();
     return applied;
 }
 
-template <int MAXC>
+template <int MAXC, bool kSh>
 static __device__ bool pass_chains8(LS& s, int lane) {
     const int k = s.k, n = s.n;
     ChainRegs c;
@@ -1014,7 +1044,7 @@ static __device__ bool pass_chains8(LS& s, int lane) {
     bool changed = false;
     while (c.locked != all) {
         const uint64_t before = c.locked;
-        if (chain_round8<MAXC>(s, c, lane)) changed = true;
+        if (chain_round8<MAXC, kSh>(s, c, lane)) changed = true;
         if (c.locked == before) break;
     }
     // back to sorted member lists; every cache of the touched groups is stale
@@ -1038,8 +1068,9 @@ static __device__ bool pass_chains8(LS& s, int lane) {
 
 // odd phase of _pass_ours: chains until every device is locked
 static __device__ __noinline__ bool pass_chains(LS& s, int lane) {
-    if (s.n <= 64 && s.k <= 8 && s.m <= 8) return pass_chains8<9>(s, lane);
-    if (s.n <= 64 && s.k <= 8 && s.m <= 15) return pass_chains8<16>(s, lane);
+    if (s.n <= 64 && s.k <= 8 && s.m <= 8) return s.w_sh ? pass_chains8<9, true>(s, lane) : pass_chains8<9, false>(s, lane);
+    if (s.n <= 64 && s.k <= 8 && s.m <= 15)
+        return s.w_sh ? pass_chains8<16, true>(s, lane) : pass_chains8<16, false>(s, lane);
     const int n = s.n;
     for (int i = lane; i < ((n + 31) >> 5); i += kWarp) s.locked[i] = 0;
     if (lane == 0) s.nlocked[0] = 0;
@@ -1360,6 +1391,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         s.m = m;
         s.cap = cap;
         s.W = SW;
+        s.w_sh = kSmemTables ? (uint32_t)__cvta_generic_to_shared(SW) : 0u;
         s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
         s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
         s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
@@ -1648,6 +1680,7 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     s.m = m;
     s.cap = cap;
     s.W = SW;
+    s.w_sh = kSmemTables ? (uint32_t)__cvta_generic_to_shared(SW) : 0u;
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
