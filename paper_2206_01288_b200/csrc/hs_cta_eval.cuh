@@ -140,12 +140,14 @@ __device__ inline CtaScratch cta_scratch_at(unsigned char* base, int k, int m) {
 // (bottleneck edges, costmodel.py:200-208, zero diagonal).  Returns datap.
 template <typename KeyT, bool kM8>
 __device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, const KeyT* RK, const double* vals,
-                                   const CtaScratch& cs, const int16_t* mem) {
+                                   const CtaScratch& cs, const int16_t* mem, int ds = 0, int rs = 0) {
+    if (!ds) ds = n;  // row strides (padded when the tables sit in shared memory)
+    if (!rs) rs = n;
     const int m = kM8 ? 8 : m_rt, km = k * m;
     for (int r = threadIdx.x; r < km; r += blockDim.x) {
         int g = r / m;
         const int16_t* gm = mem + g * m;
-        const double* row = DP + (size_t)gm[r - g * m] * n;
+        const double* row = DP + (size_t)gm[r - g * m] * ds;
         cs.rows[r] = pairwise_sum(m, [&](int c) { return row[gm[c]]; });
     }
     __syncthreads();
@@ -165,14 +167,14 @@ __device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, con
             uint32_t K[8][4];
 #pragma unroll
             for (int r = 0; r < 8; r++) {
-                const KeyT* row = RK + (size_t)A[r] * n;
+                const KeyT* row = RK + (size_t)A[r] * rs;
 #pragma unroll
                 for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[B[q]] | ((uint32_t)row[B[q + 4]] << 16);
             }
             L = Match8::solve(K);
         } else {
             L = bottleneck_threshold<uint32_t>(
-                m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
+                m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * rs + B[c]]; }, 0xffffffffu);
         }
         double v = vals[L];
         cs.E[j * kES16 + j2] = v;
@@ -191,8 +193,8 @@ __device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, con
 template <typename KeyT, bool kM8>
 __device__ inline void cta_price(int n, int k, int m_rt, const double* DP, const KeyT* RK, const double* vals,
                                  const HKBig& t, const CtaScratch& cs, double* h, const int16_t* mem, double& datap,
-                                 double& pipe) {
-    datap = cta_stage<KeyT, kM8>(n, k, m_rt, DP, RK, vals, cs, mem);
+                                 double& pipe, int ds = 0, int rs = 0) {
+    datap = cta_stage<KeyT, kM8>(n, k, m_rt, DP, RK, vals, cs, mem, ds, rs);
     pipe = cta_held_karp(k, cs.E, h, t, cs.red);
 }
 

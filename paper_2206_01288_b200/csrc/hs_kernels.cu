@@ -163,7 +163,7 @@ static int plan_for(const EvalArgs& a, const HKTables& t, int wmax, size_t smem_
     ScratchLayout wl = scratch_layout(a.k, a.m, t.hsize);
     size_t fixed = hk_bytes_host(t);
     size_t keyb = a.key16 ? 2 : 4;
-    size_t tables = (size_t)a.n * a.n * 8 + (((size_t)a.n * a.n * keyb + 15) & ~(size_t)15);
+    size_t tables = staged_table_bytes(a.n, keyb);
     *smem_tables = fixed + tables + 4 * (size_t)wl.bytes <= smem_optin;
     size_t base = fixed + (*smem_tables ? tables : 0);
     if (base + wl.bytes > smem_optin) return -2;

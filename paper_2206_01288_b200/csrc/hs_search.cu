@@ -182,7 +182,7 @@ static size_t ga_bytes(const SearchShape& sh, int W, bool smem_tables, int P, bo
     int km = sh.k * sh.m, ms = 1 + sh.max_passes;
     size_t b = sh.k <= 8 ? kHKGlobalBytes + (size_t)W * wl.bytes : al(cta_scratch_bytes(sh.k, sh.m));
     if (smem_tables)
-        b += (size_t)sh.n * sh.n * 8 + al((size_t)sh.n * sh.n * (sh.key16 ? 2 : 4)) + (size_t)sh.n * sh.n * 8;
+        b += staged_table_bytes(sh.n, sh.key16 ? 2 : 4) + (size_t)sh.n * sh.n * 8;
     size_t isl = al((size_t)ms * km * 2) + al((size_t)ms * 8) + al((size_t)P * 8) + al((size_t)km * 2) +
                  al((size_t)2 * km * 2) + al(64) + ls_bytes(sh.n, sh.k, sh.m) + al(sizeof(GAState));
     b += (warp_islands ? (size_t)W : 1) * isl;

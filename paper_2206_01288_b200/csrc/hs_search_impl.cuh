@@ -1257,7 +1257,8 @@ struct Pricer {
         if constexpr (kCta) {
             for (int i = 0; i < cnt; i++) {
                 double dp, pp;
-                cta_price<KeyT, kM8>(v.n, v.k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand + (size_t)i * km, dp, pp);
+                cta_price<KeyT, kM8>(v.n, v.k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand + (size_t)i * km, dp, pp,
+                                     v.ds, v.rs);
                 if (threadIdx.x == 0) cost[i] = dp + pp;
                 __syncthreads();
             }
@@ -1291,7 +1292,7 @@ struct Pricer {
         const int k = v.k;
         if constexpr (kCta) {
             double dp, pp;
-            cta_price<KeyT, kM8>(v.n, k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand, dp, pp);
+            cta_price<KeyT, kM8>(v.n, k, v.m, v.DP, v.RK, v.vals, hkb, cs, h, cand, dp, pp, v.ds, v.rs);
             if (threadIdx.x == 0) {
                 out3[0] = dp + pp;
                 out3[1] = dp;

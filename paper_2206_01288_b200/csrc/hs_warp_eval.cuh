@@ -46,6 +46,7 @@ __device__ __forceinline__ HKSmem hk_global(const HKTables& t, unsigned char* ba
 template <typename KeyT>
 struct EvalView {
     int n, k, m;
+    int ds, rs;  // row strides of DP / RK (padded when staged in shared memory)
     const double* DP;
     const KeyT* RK;
     const double* vals;
@@ -140,7 +141,7 @@ __device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s,
     for (int r = lane; r < km; r += kWarp) {
         int g = r / m;
         const int16_t* gm = mem + g * m;
-        const double* row = v.DP + (size_t)gm[r - g * m] * n;
+        const double* row = v.DP + (size_t)gm[r - g * m] * v.ds;
         h[r] = pairwise_sum(m, [&](int c) { return row[gm[c]]; });
     }
     __syncwarp();
@@ -164,14 +165,14 @@ __device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s,
             uint32_t K[8][4];
 #pragma unroll
             for (int r = 0; r < 8; r++) {
-                const KeyT* row = v.RK + (size_t)A[r] * n;
+                const KeyT* row = v.RK + (size_t)A[r] * v.rs;
 #pragma unroll
                 for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
             }
             L = Match8::solve(K);
         } else {
             L = bottleneck_threshold<uint32_t>(
-                m, [&](int r, int c) { return (uint32_t)v.RK[(size_t)A[r] * n + B[c]]; }, 0xffffffffu);
+                m, [&](int r, int c) { return (uint32_t)v.RK[(size_t)A[r] * v.rs + B[c]]; }, 0xffffffffu);
         }
         double val = v.vals[L];
         E[j * kES + j2] = val;
@@ -183,6 +184,20 @@ __device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s,
     double dp = s.pg[0];
     for (int g = 1; g < k; g++) dp = dmax(dp, s.pg[g]);
     datap = dp;
+}
+
+// Shared-memory row strides: an odd number of 8-byte (DP) / 4-byte (RK)
+// words per row, so lanes reading the same column of different rows hit
+// different banks (an n = 64 row is exactly 32 banks wide).
+__host__ __device__ __forceinline__ int dp_stride(int n) { return n | 1; }
+__host__ __device__ __forceinline__ int rk_stride(int n, int keyb) {
+    if (keyb == 4) return n | 1;
+    const int words = (n + 1) / 2;
+    return 2 * (words | 1);
+}
+__host__ __device__ __forceinline__ size_t staged_table_bytes(int n, int keyb) {
+    return (((size_t)n * dp_stride(n) * 8 + 15) & ~(size_t)15) +
+           (((size_t)n * rk_stride(n, keyb) * keyb + 15) & ~(size_t)15);
 }
 
 // Stage DP and the rank table into smem (or point at global copies).
@@ -197,19 +212,24 @@ __device__ inline EvalView<KeyT> stage_tables(int n, int k, int m, const double*
     v.hk = hk;
     const KeyT* grk = reinterpret_cast<const KeyT*>(rank);
     if (kSmemTables) {
+        const int ds = dp_stride(n), rs = rk_stride(n, (int)sizeof(KeyT));
         double* sdp = reinterpret_cast<double*>(smem + off);
-        off += (size_t)n * n * 8;
+        off += ((size_t)n * ds * 8 + 15) & ~(size_t)15;
         KeyT* srk = reinterpret_cast<KeyT*>(smem + off);
-        off += ((size_t)n * n * sizeof(KeyT) + 15) & ~(size_t)15;
+        off += ((size_t)n * rs * sizeof(KeyT) + 15) & ~(size_t)15;
         for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
-            sdp[i] = dp[i];
-            srk[i] = grk[i];
+            const int r = i / n, c = i - r * n;
+            sdp[r * ds + c] = dp[i];
+            srk[r * rs + c] = grk[i];
         }
         v.DP = sdp;
         v.RK = srk;
+        v.ds = ds;
+        v.rs = rs;
     } else {
         v.DP = dp;
         v.RK = grk;
+        v.ds = v.rs = n;
     }
     return v;
 }
