@@ -320,10 +320,10 @@ __device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa,
     return best;
 }
 
-__device__ __forceinline__ void invalidate(LS& s, int j) {
-    s.valid[1] &= (int)~(1u << j);
-    s.valid[2] &= (int)~(1u << j);
-    s.cver[j]++;
+__device__ __forceinline__ void invalidate(LS& s, int j) {  // atomic: sweep waves run on several warps
+    atomicAnd(&s.valid[1], (int)~(1u << j));
+    atomicAnd(&s.valid[2], (int)~(1u << j));
+    atomicAdd(&s.cver[j], 1u);
 }
 
 // ---------------------------------------------------------------------------
@@ -528,6 +528,85 @@ static __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
         }
     }
     return changed;
+}
+
+// Even phase of _pass_ours on every warp of the CTA (one island per CTA).
+// _best_candidate / _swap for pair (j, j2) read and write only groups j and
+// j2, so pairs that share no group commute: the permutation is cut into
+// waves (a pair's wave = 1 + the latest wave of an earlier pair sharing one
+// of its groups; pairs of one wave are disjoint) and each wave's pairs run
+// on different warps, with the reference's per-pair results.  Requires every
+// group at d_dp = 8 members and n <= 128 (register sweep path); called by all
+// threads, returns the same value in all of them.  Scratch: s.perm (pair
+// order by wave), s.i32 (wave starts, C(k,2) + 1 <= 3k + 8 entries), flag.
+template <bool kSh>
+static __device__ bool pass_sweep_waves(LS& s, Pcg64& rng, int wid, int lane, int W, int* flag) {
+    const int k = s.k, np = k * (k - 1) / 2;
+    int16_t* order = s.perm + np;  // s.perm holds k*k + cap entries
+    int* wstart = s.i32;
+    if (wid == 0 && lane == 0) {
+        int ok = 1;
+        for (int j = 0; j < k; j++) ok &= s.sz[j] == 8;
+        flag[1] = ok;
+    }
+    __syncthreads();
+    if (!flag[1]) {  // unbalanced groups: the sequential sweep on the driver warp
+        if (wid == 0) {
+            const bool ch = pass_sweep(s, rng, lane);
+            if (lane == 0) flag[0] = ch;
+        }
+        __syncthreads();
+        return flag[0] != 0;
+    }
+    if (wid == 0 && lane == 0) {
+        int16_t* perm = s.perm;
+        for (int i = 0; i < np; i++) perm[i] = (int16_t)i;
+        for (int i = np - 1; i >= 1; i--) {
+            int jx = (int)rng.interval((uint64_t)i);
+            int16_t t = perm[i];
+            perm[i] = perm[jx];
+            perm[jx] = t;
+        }
+        int ready[16], wave[120], cnt[121];
+        for (int j = 0; j < k; j++) ready[j] = 0;
+        int nw = 0;
+        for (int q = 0; q < np; q++) {
+            int j, j2;
+            decode_pair(perm[q], k, j, j2);
+            const int w = max(ready[j], ready[j2]);
+            wave[q] = w;
+            ready[j] = ready[j2] = w + 1;
+            nw = max(nw, w + 1);
+        }
+        for (int w = 0; w <= nw; w++) cnt[w] = 0;
+        for (int q = 0; q < np; q++) cnt[wave[q] + 1]++;
+        for (int w = 0; w < nw; w++) cnt[w + 1] += cnt[w];
+        for (int w = 0; w <= nw; w++) wstart[w] = cnt[w];
+        for (int q = 0; q < np; q++) order[cnt[wave[q]]++] = perm[q];  // stable: permutation order inside a wave
+        wstart[np + 1] = nw;
+        *flag = 0;
+    }
+    __syncthreads();
+    uint32_t pi = 0, pl = 1;
+    if (lane < 28) {
+        int i = 0, t = lane;
+        while (t >= 7 - i) {
+            t -= 7 - i;
+            i++;
+        }
+        pi = (uint32_t)i;
+        pl = (uint32_t)(i + 1 + t);
+    }
+    const int nw = wstart[np + 1];
+    for (int w = 0; w < nw; w++) {
+        for (int x = wstart[w] + wid; x < wstart[w + 1]; x += W) {
+            int j, j2;
+            decode_pair(order[x], k, j, j2);
+            if (sweep_pair8<kSh>(s, j, j2, lane, pi, pl) && lane == 0) atomicOr(flag, 1);
+        }
+        __syncthreads();
+    }
+    return *flag != 0;
 }
 
 // _home_costs (:287-291) for every group whose members changed
@@ -1508,6 +1587,9 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
 
     const int gen_end = min(a.gen_end, a.generations);
     const int stop_after = a.kind == 0 ? 2 : 1;
+    // CTA-mode islands with the register sweep path run the even passes as
+    // waves over all warps (balanced groups are checked per pass below)
+    const bool waves = !kWI && !kCta && a.kind == 0 && m == 8 && n <= 128 && W > 1;
     while (!g.ctl[1] && g.ctl[2] < gen_end) {
         const int gen = g.ctl[2];
         if (driver) {
@@ -1527,7 +1609,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             long long t1 = clock64();
             if (a.prof && isl == 0 && lane == 0) a.prof[0] += t1 - t0;
             int nsnap = 1;
-            if (a.kind != 2) {  // _refine (:455-487)
+            if (a.kind != 2 && !waves) {  // _refine (:455-487)
                 load_groups(s, g.snaps, lane);
                 int stale = 0;
                 for (int t = 0; t < a.max_passes; t++) {
@@ -1549,7 +1631,41 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
                     nsnap++;
                 }
             }
+            if (waves) load_groups(s, g.snaps, lane);
             if (lane == 0) g.ctl[0] = nsnap;
+        }
+        if (waves) {
+            // _refine with the even passes spread over the CTA's warps; the
+            // odd passes (chains) stay on the driver warp
+            island_sync();
+            int nsnap = 1, stale = 0;
+            for (int t = 0; t < a.max_passes; t++) {
+                long long p0 = clock64();
+                bool changed;
+                if (t % 2 == 0) {
+                    changed = s.w_sh ? pass_sweep_waves<true>(s, rng, wid, lane, W, g.ctl + 3)
+                                     : pass_sweep_waves<false>(s, rng, wid, lane, W, g.ctl + 3);
+                } else {
+                    if (driver) {
+                        const bool ch = pass_chains(s, lane);
+                        if (lane == 0) g.ctl[3] = ch;
+                    }
+                    __syncthreads();
+                    changed = g.ctl[3] != 0;
+                }
+                long long p1 = clock64();
+                if (a.prof && isl == 0 && threadIdx.x == 0) a.prof[1 + (t & 1)] += p1 - p0;
+                __syncthreads();  // every thread has read the flag before it is reused
+                if (!changed) {
+                    stale++;
+                    if (stale >= stop_after) break;
+                    continue;
+                }
+                stale = 0;
+                if (driver) store_groups(s, g.snaps + (size_t)nsnap * km, lane);
+                nsnap++;
+            }
+            if (threadIdx.x == 0) g.ctl[0] = nsnap;
         }
         long long q0 = clock64();
         island_sync();
