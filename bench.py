@@ -282,12 +282,16 @@ def run_ours():
     achieved = SMEM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak = SMEM_BYTES_PER_CLK_SM * sms * sm_mhz * 1e6 / 1e9
-    traffic, traffic_src, smem_wf = None, None, None
+    traffic, traffic_src, smem_wf, pipes = None, None, None, None
     tp = ROOT / "profiles" / "eval_traffic.json"
     if tp.exists():  # ncu --set full capture of this kernel (scripts/gpu_ncu.sh)
         tj = json.loads(tp.read_text())
         traffic = tj["dram_bytes_per_launch"] * P / tj["population"]
         smem_wf = tj["smem_wavefronts_per_launch"] * 128 * P / tj["population"]
+        if "alu_pipe_pct" in tj:  # the pipe that actually binds this issue-bound kernel
+            pipes = {"bound": "alu pipe (instruction issue)", "alu_pipe_frac": tj["alu_pipe_pct"] / 100.0,
+                     "issue_slots_frac": tj["issue_active_pct"] / 100.0, "ipc": tj["ipc"],
+                     "smem_pipe_frac": tj["smem_pipe_pct"] / 100.0, "source": tj["source"]}
         traffic_src = (f"{tj['source']}: dram__bytes_read.sum + dram__bytes_write.sum at P={tj['population']}"
                        + ("" if tj["population"] == P else f", scaled to P={P}")
                        + f"; algorithmic HBM bytes per launch = {HBM_BYTES_PER_EVAL * P}")
@@ -301,7 +305,7 @@ def run_ours():
                    "parallelism": f"population sharded over {world} GPU(s), no data-path collective"},
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
-                     "smem_wavefront_bytes": smem_wf,
+                     "smem_wavefront_bytes": smem_wf, "pipes": pipes,
                      "per_eval_bytes": SMEM_BYTES_PER_EVAL, "kernel": "eval_warp_kernel", "kernel_ms": kern_ms,
                      "peak_source": f"architectural 128 B/clk/SM x {sms} SMs at the {sm_mhz:.0f} MHz SM clock "
                                     "sampled during this run (MEASURED_PEAKS.json has no smem figure)",

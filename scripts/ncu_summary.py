@@ -125,6 +125,10 @@ if os.path.exists(rp):
                        "smem_wavefronts_per_launch": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", {}),
                        "warp_instructions_per_launch": num("smsp__inst_executed.sum", {}) if "smsp__inst_executed.sum" in rec else None,
                        "duration_ms": num("gpu__time_duration.sum", {"ms": 1.0, "us": 1e-3, "ns": 1e-6}),
+                       "alu_pipe_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", {}),
+                       "issue_active_pct": num("sm__issue_active.avg.pct_of_peak_sustained_elapsed", {}),
+                       "ipc": num("sm__inst_executed.avg.per_cycle_active", {}),
+                       "smem_pipe_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", {}),
                        "source": f"profiles/{tag}_ncu.md (ncu --set full --clock-control none, one launch)"},
                       open(os.path.join(ROOT, "profiles", "eval_traffic.json"), "w"), indent=1)
 os.makedirs(os.path.dirname(out_md), exist_ok=True)
