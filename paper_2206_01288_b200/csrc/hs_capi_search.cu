@@ -211,10 +211,8 @@ int hs_ga_result(hs_ga* ga, int16_t* best_groups, double* best3, double* best_pe
         fprintf(stderr,
                 "[hs_ga_profile] cycles: crossover %lld sweep %lld chains %lld price %lld | chain rounds %lld "
                 "(caches at start %lld) moves %lld (cache refresh %lld) | best_candidate %lld calls %lld cycles, "
-                "swaps %lld, fast_edge computes %lld (%lld cycles) | register chains: start %lld, steps %lld, "
-                "closure %lld\n",
-                pv[0], pv[1], pv[2], pv[3], pv[5], pv[4], pv[7], pv[6], pv[8], pv[12], pv[11], pv[10], pv[9], pv[13],
-                pv[14], pv[15]);
+                "swaps %lld, fast_edge computes %lld (%lld cycles)\n",
+                pv[0], pv[1], pv[2], pv[3], pv[5], pv[4], pv[7], pv[6], pv[8], pv[12], pv[11], pv[10], pv[9]);
     }
     for (int i = 0; i < I; i++) {
         if (trace_len) trace_len[i] = st[i].gen;

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
     const int rank = (int)cl.block_rank(), cs = t.cs;
     double* buf[2] = {sm2, sm2 + t.Cmax};
     double* Es = sm2 + 2 * t.Cmax;
-    __shared__ double* rb[2][8];
+    __shared__ double* rb[2][16];
     if (threadIdx.x < cs) {
         rb[0][threadIdx.x] = cl.map_shared_rank(buf[0], (int)threadIdx.x);
         rb[1][threadIdx.x] = cl.map_shared_rank(buf[1], (int)threadIdx.x);
@@ -262,14 +262,18 @@ int get_hk_two(int device, int k, HKTwo* out) {
         for (int p = 2; p <= k; p++) maxS = std::max<uint64_t>(maxS, size[p]);
         DeviceHKTwo d;
         d.t.cs = 0;
-        for (int cs = 1; cs <= 8; cs *= 2) {
-            const uint64_t C = (maxS + cs - 1) / cs;
-            if ((2 * C + 16 * kES16) * 8 + 1024 <= (uint64_t)optin) {
-                d.t.cs = cs;
-                break;
+        // smallest cluster whose CTAs fit two per SM (32 resident warps);
+        // failing that, the smallest that fits one per SM
+        for (int pass = 0; pass < 2 && !d.t.cs; pass++) {
+            const uint64_t budget = pass == 0 ? (uint64_t)optin / 2 - 2048 : (uint64_t)optin - 1024;
+            for (int cs = 1; cs <= 16; cs *= 2) {
+                const uint64_t C = (maxS + cs - 1) / cs;
+                if ((2 * C + 16 * kES16) * 8 <= budget) {
+                    d.t.cs = cs;
+                    break;
+                }
             }
         }
-        if (!d.t.cs) return -3;
         const int cs = d.t.cs;
         d.t.Cmax = 0;
         for (int p = 0; p < 18; p++) {
@@ -284,7 +288,7 @@ int get_hk_two(int device, int k, HKTwo* out) {
         std::vector<std::vector<uint64_t>> per(cs);
         std::vector<std::vector<uint32_t>> perd(cs);
         for (int p = 0; p < 18; p++) {
-            for (int q = 0; q < 9; q++) d.t.rbeg[p][q] = (int)rws.size();
+            for (int q = 0; q < 17; q++) d.t.rbeg[p][q] = (int)rws.size();
             if (p < 2 || p > k) continue;
             for (int q = 0; q < cs; q++) {
                 per[q].clear();
@@ -319,7 +323,7 @@ int get_hk_two(int device, int k, HKTwo* out) {
                 for (uint64_t w : per[q]) rws.push_back(w + (base << 34));
                 dws.insert(dws.end(), perd[q].begin(), perd[q].end());
             }
-            for (int q = cs; q < 9; q++) d.t.rbeg[p][q] = (int)rws.size();
+            for (int q = cs; q < 17; q++) d.t.rbeg[p][q] = (int)rws.size();
         }
         if (cudaMalloc(&d.rw, rws.size() * 8) != cudaSuccess) return -1;
         if (cudaMalloc(&d.dw, dws.size() * 4) != cudaSuccess) return -1;
@@ -333,11 +337,41 @@ int get_hk_two(int device, int k, HKTwo* out) {
     return 0;
 }
 
+static cudaLaunchConfig_t cluster_cfg(const HKTwo& t, unsigned grid, cudaStream_t s, cudaLaunchAttribute* at) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kClusterThreads, 1, 1);
+    cfg.dynamicSmemBytes = cluster_smem_bytes(t);
+    cfg.stream = s;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)t.cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
+static int set_cluster_attrs(const HKTwo& t) {
+    if (cudaFuncSetAttribute(hk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)cluster_smem_bytes(t)) != cudaSuccess)
+        return -1;
+    if (t.cs > 8 && cudaFuncSetAttribute(hk_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                        cudaSuccess)
+        return -1;
+    return 0;
+}
+
 int cluster_grid(const HKTwo& t, int sm_count) {
-    const size_t smem = cluster_smem_bytes(t) + 256;
-    int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, (228u << 10) / smem));
-    if (t.cs > 1) per_sm = 1;
-    return std::max(1, sm_count / t.cs) * t.cs * per_sm;
+    if (set_cluster_attrs(t)) return t.cs;
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = cluster_cfg(t, (unsigned)(sm_count * 4 / t.cs * t.cs), 0, at);
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, hk_cluster_kernel, &cfg) != cudaSuccess || clusters < 1) {
+        cudaGetLastError();
+        clusters = std::max(1, sm_count / t.cs);
+    }
+    return clusters * t.cs;
 }
 
 template <typename KT, bool M8>
@@ -363,22 +397,9 @@ int launch_hk_cluster(const double* E, int es, int64_t estride, int k, int64_t B
                       const double* add, const uint8_t* bad, double* out_total, double* out_pipe, cudaStream_t s) {
     if (B == 0) return 0;
     const int clusters = (int)std::min<int64_t>(grid / t.cs, B);
-    const size_t smem = cluster_smem_bytes(t);
-    if (cudaFuncSetAttribute(hk_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-        return -1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(clusters * t.cs), 1, 1);
-    cfg.blockDim = dim3(kClusterThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
+    if (set_cluster_attrs(t)) return -1;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)t.cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cudaLaunchConfig_t cfg = cluster_cfg(t, (unsigned)(clusters * t.cs), s, at);
     if (cudaLaunchKernelEx(&cfg, hk_cluster_kernel, E, es, estride, k, B, t, add, bad, out_total, out_pipe) !=
         cudaSuccess)
         return -1;

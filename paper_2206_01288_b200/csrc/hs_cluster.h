@@ -22,22 +22,22 @@ constexpr int kStageStride = 16 * kStageES;   // doubles per staged candidate
 //   rwords[i]: r (16) | local slot of h[r][first member] (17) << 16 |
 //              "h[r][.] runs into the next CTA's slice" (1) << 33 |
 //              index of r's first destination word (30) << 34
-//   dwords[j]: destination CTA (3) << 17 | local slot (17), one per u not in
+//   dwords[j]: destination CTA (4) << 17 | local slot (17), one per u not in
 //              r, ascending u
 // The sources of layer p on CTA q are rwords[rbeg[p][q] .. rbeg[p][q + 1]).
 struct HKTwo {
     const uint64_t* rwords;
     const uint32_t* dwords;
-    int rbeg[18][9];
+    int rbeg[18][17];
     int C[18];    // slice length per layer
     int Cmax;     // buffer length (max over layers)
-    int cs;       // CTAs per cluster (1, 2, 4 or 8)
+    int cs;       // CTAs per cluster (1, 2, 4, 8 or 16)
 };
 
 int get_hk_two(int device, int k, HKTwo* out);
 size_t cluster_smem_bytes(const HKTwo& t);
 // grid in CTAs for one pricing launch (a multiple of t.cs)
-int cluster_grid(const HKTwo& t, int sm_count);
+int cluster_grid(const HKTwo& t, int sm_count);  // CTAs: co-resident clusters x cs
 
 // Stage kernel: validation, datap / per_group and the padded stage graph
 // E[b] (16 x 17 doubles) of partitions [0, P) of a.groups; bad[b] = 1 for

@@ -976,7 +976,6 @@ template <int MAXC, bool kSh>
 static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     const int k = s.k;
     const WTab<kSh> W = wtab<kSh>(s);
-    const long long c0 = g_prof ? clock64() : 0;
     refresh_homes<MAXC, kSh>(W, c, lane);
     // fastest_free of every group at once: three REDUX stages, 8 groups wide
     int vv[8];
@@ -1036,11 +1035,6 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     const bool take1 = u1 && (!u0 || gsl[1] > gsl[0]);
     double best;
     const int start0 = redux_argmax(take1 ? gsl[1] : gsl[0], u0 || u1, take1 ? isl[1] : isl[0], best);
-    const long long c1 = g_prof ? clock64() : 0;
-    if (g_prof && lane == 0) {
-        g_prof[13] += c1 - c0;
-        g_prof[4] += 1;
-    }
     if (start0 == 0x7FFFFFFF) return false;
     const int start = start0;
     int* mv_v = s.i32;
@@ -1078,11 +1072,6 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         }
     }
     __syncwarp();
-    const long long c2 = g_prof ? clock64() : 0;
-    if (g_prof && lane == 0) {
-        g_prof[14] += c2 - c1;
-        g_prof[7] += nm;
-    }
     double prefix = 0.0, best_v = -kInf;
     int best_l = -1;
     for (int l = 0; l < nm; l++) {  // prefix[l] = cumsum of steps[0..l-1]
@@ -1102,7 +1091,6 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     for (int t = nm - 1; t >= keep; t--) cmove<kSh>(W, c, mv_v[t], mv_dst[t], mv_src[t], lane);
     if (applied && best_l < nm) cmove<kSh>(W, c, mv_v[best_l], mv_src[best_l], start, lane);
     __syncwarp();
-    if (g_prof && lane == 0) g_prof[15] += clock64() - c2;
     return applied;
 }
 
