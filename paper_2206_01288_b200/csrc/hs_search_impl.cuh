@@ -320,7 +320,14 @@ __device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa,
     return best;
 }
 
-__device__ __forceinline__ void invalidate(LS& s, int j) {  // atomic: sweep waves run on several warps
+__device__ __forceinline__ void invalidate(LS& s, int j) {
+    s.valid[1] &= (int)~(1u << j);
+    s.valid[2] &= (int)~(1u << j);
+    s.cver[j]++;
+}
+
+// same, safe when several warps finish pairs at once (sweep waves)
+__device__ __forceinline__ void invalidate_atomic(LS& s, int j) {
     atomicAnd(&s.valid[1], (int)~(1u << j));
     atomicAnd(&s.valid[2], (int)~(1u << j));
     atomicAdd(&s.cver[j], 1u);
@@ -466,8 +473,8 @@ static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, 
         if (lane < 8) wj[lane] = (int16_t)byte_of(X, lane);
         else if (lane < 16) wj2[lane - 8] = (int16_t)byte_of(Y, lane - 8);
         if (lane == 0) {
-            invalidate(s, j);
-            invalidate(s, j2);
+            invalidate_atomic(s, j);
+            invalidate_atomic(s, j2);
         }
         __syncwarp();
     }
