@@ -728,6 +728,7 @@ void orc_crossover(const int32_t *p1, const int32_t *p2, int k, int m, orc_pcg64
 
 static double row_pw_sum(const double *w, int n, int32_t u, const int32_t *grp, int cnt) {
     double buf[1024];
+    if (cnt <= 0) return 0.0; /* numpy: the sum of an empty selection */
     for (int i = 0; i < cnt; i++) buf[i] = w[(size_t)u * n + grp[i]];
     return pw_sum(buf, cnt);
 }
