@@ -418,7 +418,7 @@ __device__ __forceinline__ void fast_edges8(const WTab<kSh>& W, uint64_t X, uint
 
 // the `for _ in range(d_dp)` loop of _pass_ours for pair (j, j2); true if a
 // swap was applied
-template <bool kSh>
+template <bool kSh, bool kAtomic = false>
 static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, uint32_t pl) {
     const WTab<kSh> W = wtab<kSh>(s);
     const int16_t* gj = s.G + j * s.cap;
@@ -473,8 +473,13 @@ static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, 
         if (lane < 8) wj[lane] = (int16_t)byte_of(X, lane);
         else if (lane < 16) wj2[lane - 8] = (int16_t)byte_of(Y, lane - 8);
         if (lane == 0) {
-            invalidate_atomic(s, j);
-            invalidate_atomic(s, j2);
+            if (kAtomic) {  // sweep waves: other warps finish their pairs at the same time
+                invalidate_atomic(s, j);
+                invalidate_atomic(s, j2);
+            } else {
+                invalidate(s, j);
+                invalidate(s, j2);
+            }
         }
         __syncwarp();
     }
@@ -609,7 +614,7 @@ static __device__ bool pass_sweep_waves(LS& s, Pcg64& rng, int wid, int lane, in
         for (int x = wstart[w] + wid; x < wstart[w + 1]; x += W) {
             int j, j2;
             decode_pair(order[x], k, j, j2);
-            if (sweep_pair8<kSh>(s, j, j2, lane, pi, pl) && lane == 0) atomicOr(flag, 1);
+            if (sweep_pair8<kSh, true>(s, j, j2, lane, pi, pl) && lane == 0) atomicOr(flag, 1);
         }
         __syncthreads();
     }
@@ -1049,6 +1054,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     int* mv_dst = s.i32 + 2 * k;
     double* steps = s.f64;
     double* closers = s.f64 + k + 1;
+    const ChainRegs snap = c;  // pre-chain state: restoring it undoes every move at once
     int cur = start, nm = 0;
     bool natural = false;
     for (int it = 0; it < k; it++) {
@@ -1094,8 +1100,19 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         best_l = nm;
     }
     const bool applied = best_v > 0.0;
+    // Outcome: moves[0 .. best_l) kept and moves[best_l]'s device sent back to
+    // start (if best_l < nm), or nothing kept.  Reach it from whichever end
+    // needs fewer moves: undo the tail, or restore the snapshot and replay the
+    // kept prefix (home costs are exact minima either way; locks stay).
     const int keep = applied ? best_l : 0;
-    for (int t = nm - 1; t >= keep; t--) cmove<kSh>(W, c, mv_v[t], mv_dst[t], mv_src[t], lane);
+    if (keep < nm - keep) {
+        const uint64_t locked = c.locked;
+        c = snap;
+        c.locked = locked;
+        for (int t = 0; t < keep; t++) cmove<kSh>(W, c, mv_v[t], mv_src[t], mv_dst[t], lane);
+    } else {
+        for (int t = nm - 1; t >= keep; t--) cmove<kSh>(W, c, mv_v[t], mv_dst[t], mv_src[t], lane);
+    }
     if (applied && best_l < nm) cmove<kSh>(W, c, mv_v[best_l], mv_src[best_l], start, lane);
     __syncwarp();
     return applied;
