@@ -989,32 +989,29 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     const int k = s.k;
     const WTab<kSh> W = wtab<kSh>(s);
     refresh_homes<MAXC, kSh>(W, c, lane);
-    // fastest_free of every group at once: three REDUX stages, 8 groups wide
-    int vv[8];
-    double hh[8];
-    {
-        uint32_t hi[8], lo[8], mh[8], ml[8];
-        int id[8];
-        bool ok[8];
+    // fastest_free (:318-328) of every group: lane i scans group i's packed
+    // members (ascending, so a strict '<' keeps the smallest id on ties)
+    // against the home costs published in shared memory
+    double* hs = s.home;  // n doubles, otherwise unused on this path
+    hs[lane] = c.h0;
+    if (lane + 32 < s.n) hs[lane + 32] = c.h1;
+    __syncwarp();
+    int myv = -1;
+    double myh = 0.0;
+    if (lane < k) {
+        const int cnt = __popcll(c.GM);
+        if (cnt >= 2) {
 #pragma unroll
-        for (int i = 0; i < 8; i++) {
-            double h;
-            ok[i] = i < k && lane_free(c, i, lane, h, id[i]);
-            const uint64_t key = ok[i] ? ord_bits(h) : ~0ull;
-            hi[i] = (uint32_t)(key >> 32);
-            lo[i] = (uint32_t)key;
-        }
-#pragma unroll
-        for (int i = 0; i < 8; i++) mh[i] = __reduce_min_sync(kFull, hi[i]);
-#pragma unroll
-        for (int i = 0; i < 8; i++) ml[i] = __reduce_min_sync(kFull, hi[i] == mh[i] ? lo[i] : 0xFFFFFFFFu);
-#pragma unroll
-        for (int i = 0; i < 8; i++) {
-            const int v = (int)__reduce_min_sync(
-                kFull, (ok[i] && hi[i] == mh[i] && lo[i] == ml[i]) ? (unsigned)id[i] : 0x7FFFFFFFu);
-            const int cnt = __popcll(shfl64(c.GM, i & 31));
-            vv[i] = (i >= k || cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
-            hh[i] = from_ord(((uint64_t)mh[i] << 32) | ml[i]);
+            for (int t = 0; t < MAXC; t++) {
+                const uint32_t d = mbyte(c.L, t);
+                if (t < cnt && !(c.locked >> d & 1ull)) {
+                    const double h = hs[d];
+                    if (myv < 0 || h < myh) {
+                        myv = (int)d;
+                        myh = h;
+                    }
+                }
+            }
         }
     }
     // gain_i = max_{j != i} mean[v_i, j] - home_i for (i, j) = (e >> 3, e & 7),
@@ -1026,14 +1023,8 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
 #pragma unroll
     for (int sl = 0; sl < 2; sl++) {
         const int i = (lane >> 3) + 4 * sl, j = lane & 7;
-        int vi = -1;
-        double hi = 0.0;
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-            if (q == i) {
-                vi = vv[q];
-                hi = hh[q];
-            }
+        const int vi = __shfl_sync(kFull, myv, i);
+        const double hi = __shfl_sync(kFull, myh, i);
         double x = -kInf;
         if (j < k && j != i && vi >= 0) x = members_mean<MAXC, kSh>(W, W.row((uint32_t)vi), Lj, cj);
         x = dmax(x, __shfl_xor_sync(kFull, x, 1));
