@@ -1018,7 +1018,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     // e = lane + 32 sl: row maxima inside 8-lane segments
     const Members Lj = shfl_members(c.L, lane & 7);
     const int cj = __popcll(shfl64(c.GM, lane & 7));
-    double gsl[2];
+    double gsl[2], mrow[2];
     int isl[2];
 #pragma unroll
     for (int sl = 0; sl < 2; sl++) {
@@ -1027,6 +1027,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         const double hi = __shfl_sync(kFull, myh, i);
         double x = -kInf;
         if (j < k && j != i && vi >= 0) x = members_mean<MAXC, kSh>(W, W.row((uint32_t)vi), Lj, cj);
+        mrow[sl] = x;  // mean[v_i, j], reused by the chain's first step when i = start
         x = dmax(x, __shfl_xor_sync(kFull, x, 1));
         x = dmax(x, __shfl_xor_sync(kFull, x, 2));
         x = dmax(x, __shfl_xor_sync(kFull, x, 4));
@@ -1049,13 +1050,21 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
     int cur = start, nm = 0;
     bool natural = false;
     for (int it = 0; it < k; it++) {
-        refresh_homes<MAXC, kSh>(W, c, lane);
-        double home;
-        const int v = chain_fastest_free(c, cur, lane, home);
-        if (v < 0) break;
-        // scores = mean[v, targets]; dst = first maximum
-        double mj = 0.0;
-        if (lane < k) mj = members_mean<MAXC, kSh>(W, W.row((uint32_t)v), c.L, __popcll(c.GM));
+        double home, mj = 0.0;
+        int v;
+        if (it == 0) {
+            // nothing moved since the start selection: its fastest free device
+            // of the start group and that device's means are the step's own
+            v = __shfl_sync(kFull, myv, start);
+            home = __shfl_sync(kFull, myh, start);
+            mj = __shfl_sync(kFull, start < 4 ? mrow[0] : mrow[1], 8 * (start & 3) + (lane & 7));
+        } else {
+            refresh_homes<MAXC, kSh>(W, c, lane);
+            v = chain_fastest_free(c, cur, lane, home);
+            if (v < 0) break;
+            // scores = mean[v, targets]; dst = first maximum
+            if (lane < k) mj = members_mean<MAXC, kSh>(W, W.row((uint32_t)v), c.L, __popcll(c.GM));
+        }
         double sc;
         const int dst = redux_argmax(mj, lane < k && lane != cur, lane, sc);
         const double mstart = __shfl_sync(kFull, mj, start);
