@@ -1085,6 +1085,12 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         }
     }
     __syncwarp();
+    if (nm == 1) {  // closers[0] is -inf and a single move cannot close the cycle: rejected
+        const uint64_t locked = c.locked;
+        c = snap;
+        c.locked = locked;
+        return false;
+    }
     double prefix = 0.0, best_v = -kInf;
     int best_l = -1;
     for (int l = 0; l < nm; l++) {  // prefix[l] = cumsum of steps[0..l-1]
