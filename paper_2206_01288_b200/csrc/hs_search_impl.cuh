@@ -1059,6 +1059,8 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
             home = __shfl_sync(kFull, myh, start);
             mj = __shfl_sync(kFull, start < 4 ? mrow[0] : mrow[1], 8 * (start & 3) + (lane & 7));
         } else {
+            const uint64_t gm = shfl64(c.GM, cur);
+            if (__popcll(gm) < 2 || !(gm & ~c.locked)) break;  // fastest_free(cur) is None
             refresh_homes<MAXC, kSh>(W, c, lane);
             v = chain_fastest_free(c, cur, lane, home);
             if (v < 0) break;
