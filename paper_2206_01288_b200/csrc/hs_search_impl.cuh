@@ -1069,6 +1069,13 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         }
         double sc;
         const int dst = redux_argmax(mj, lane < k && lane != cur, lane, sc);
+        if (it == 0 && !(shfl64(c.GM, dst) & ~c.locked)) {
+            // dst has no free device even before v arrives (v will be locked), so
+            // the chain ends after this move, and a single move is always rejected
+            // (see below): the round's only effect is locking v
+            c.locked |= 1ull << v;
+            return false;
+        }
         const double mstart = __shfl_sync(kFull, mj, start);
         if (lane == 0) {
             closers[nm] = cur != start ? mstart - home : -kInf;
