@@ -984,21 +984,37 @@ __device__ __forceinline__ int chain_fastest_free(const ChainRegs& c, int i, int
     return (cnt < 2 || v == 0x7FFFFFFF) ? -1 : v;
 }
 
+// Start-selection state carried from one chain round to the next.  A round
+// whose only effect is locking the start group's device (no move survives)
+// leaves every other group's fastest free device, its means and the home
+// costs unchanged, so the next round recomputes only that group's row.
+struct RoundCache {
+    int row;  // -1: recompute every row; else only this group's row
+    int myv;
+    double myh, mrow[2];
+};
+
 template <int MAXC, bool kSh>
-static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
+static __device__ bool chain_round8(LS& s, ChainRegs& c, RoundCache& rc, int lane) {
     const int k = s.k;
     const WTab<kSh> W = wtab<kSh>(s);
+    const int row = rc.row;
+    rc.row = -1;
     refresh_homes<MAXC, kSh>(W, c, lane);
     // fastest_free (:318-328) of every group: lane i scans group i's packed
     // members (ascending, so a strict '<' keeps the smallest id on ties)
     // against the home costs published in shared memory
     double* hs = s.home;  // n doubles, otherwise unused on this path
-    hs[lane] = c.h0;
-    if (lane + 32 < s.n) hs[lane + 32] = c.h1;
-    __syncwarp();
-    int myv = -1;
-    double myh = 0.0;
-    if (lane < k) {
+    if (row < 0) {
+        hs[lane] = c.h0;
+        if (lane + 32 < s.n) hs[lane + 32] = c.h1;
+        __syncwarp();
+    }
+    int myv = rc.myv;
+    double myh = rc.myh;
+    if (lane < k && (row < 0 || lane == row)) {
+        myv = -1;
+        myh = 0.0;
         const int cnt = __popcll(c.GM);
         if (cnt >= 2) {
 #pragma unroll
@@ -1025,8 +1041,11 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         const int i = (lane >> 3) + 4 * sl, j = lane & 7;
         const int vi = __shfl_sync(kFull, myv, i);
         const double hi = __shfl_sync(kFull, myh, i);
-        double x = -kInf;
-        if (j < k && j != i && vi >= 0) x = members_mean<MAXC, kSh>(W, W.row((uint32_t)vi), Lj, cj);
+        double x = rc.mrow[sl];
+        if (row < 0 || i == row) {
+            x = -kInf;
+            if (j < k && j != i && vi >= 0) x = members_mean<MAXC, kSh>(W, W.row((uint32_t)vi), Lj, cj);
+        }
         mrow[sl] = x;  // mean[v_i, j], reused by the chain's first step when i = start
         x = dmax(x, __shfl_xor_sync(kFull, x, 1));
         x = dmax(x, __shfl_xor_sync(kFull, x, 2));
@@ -1074,6 +1093,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
             // the chain ends after this move, and a single move is always rejected
             // (see below): the round's only effect is locking v
             c.locked |= 1ull << v;
+            rc = RoundCache{start, myv, myh, {mrow[0], mrow[1]}};
             return false;
         }
         const double mstart = __shfl_sync(kFull, mj, start);
@@ -1098,6 +1118,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, int lane) {
         const uint64_t locked = c.locked;
         c = snap;
         c.locked = locked;
+        rc = RoundCache{start, myv, myh, {mrow[0], mrow[1]}};  // as a lock-only round
         return false;
     }
     double prefix = 0.0, best_v = -kInf;
@@ -1158,11 +1179,12 @@ static __device__ bool pass_chains8(LS& s, int lane) {
     c.h0 = c.h1 = kInf;
     c.st0 = c.st1 = true;
     c.locked = 0;
+    RoundCache rc{-1, -1, 0.0, {0.0, 0.0}};
     const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
     bool changed = false;
     while (c.locked != all) {
         const uint64_t before = c.locked;
-        if (chain_round8<MAXC, kSh>(s, c, lane)) changed = true;
+        if (chain_round8<MAXC, kSh>(s, c, rc, lane)) changed = true;
         if (c.locked == before) break;
     }
     // back to sorted member lists; every cache of the touched groups is stale
