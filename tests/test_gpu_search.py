@@ -303,3 +303,19 @@ def test_local_search_driver_shapes_vs_oracle(n, k, m):
         out = S.local_search(g, w, p, kind="ours", rng=r1)
         want = O.Oracle.of(g, w).local_search(np.array(p.groups, dtype=np.int32), "ours", st)
         assert [list(x) for x in out.groups] == want.tolist()
+
+
+@pytest.mark.parametrize("case", [2, 4, 5])
+@pytest.mark.parametrize("seed", [11, 12, 13, 14])
+def test_evolve_paper_shape_seeds_vs_oracle(case, seed):
+    """The paper shape (64 devices, 8x8) over several seeds: every chain-round
+    shortcut (single-move rejection, lock-only rounds, prefix replay) and the
+    sweep waves against the oracle's evolve, traces included."""
+    g, w = I.instance(f"case{case}")
+    cfg = S.ScheduleConfig(pop_size=16, generations=40, local_search="ours", seed=seed)
+    r = S.evolve(g, w, cfg)
+    o = O.Oracle.of(g, w).evolve(16, 40, "ours", seed=seed)
+    assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+    assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+    assert [t[1] for t in r.trace] == list(o["trace_best"])
+    assert [t[2] for t in r.trace] == list(o["trace_mean"])
