@@ -449,15 +449,14 @@ static __device__ bool sweep_pair8(LS& s, int j, int j2, int lane, uint32_t pi, 
         const double t1a = __shfl_sync(kFull, t, 0), t1b = __shfl_sync(kFull, t, 1);
         const double t2a = __shfl_sync(kFull, t, 2), t2b = __shfl_sync(kFull, t, 3);
         // _best_candidate: (d1,d1p), (d1,d2p), (d2,d1p), (d2,d2p), first best
-        const double g[4] = {t1a + t2a, t1a + t2b, t1b + t2a, t1b + t2b};
-        double best = -kInf;
-        int bc = 0;
-#pragma unroll
-        for (int c = 0; c < 4; c++)
-            if (g[c] > best) {
-                best = g[c];
-                bc = c;
-            }
+        // (gains are finite, so a two-level tree that keeps the left operand
+        // on ties is the sequential "first strictly greater" scan)
+        const double g0 = t1a + t2a, g1 = t1a + t2b, g2 = t1b + t2a, g3 = t1b + t2b;
+        const bool s01 = g1 > g0, s23 = g3 > g2;
+        const double b01 = s01 ? g1 : g0, b23 = s23 ? g3 : g2;
+        const bool right = b23 > b01;
+        const double best = right ? b23 : b01;
+        const int bc = right ? (s23 ? 3 : 2) : (s01 ? 1 : 0);
         if (!(best > 0.0)) break;
         const uint32_t pa = (bc < 2) ? (cx >> 3) : (cx & 7);      // a = d1 or d2 in group j
         const uint32_t pb = (bc & 1) ? (cy & 7) : (cy >> 3);      // b = d1p or d2p in group j2
