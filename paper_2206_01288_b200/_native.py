@@ -17,6 +17,9 @@ import numpy as np
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libhetsched_sm100a.so"
+# experiments only: load an alternative build of the same sources
+if os.environ.get("HS_LIB_PATH"):
+    LIB_PATH = Path(os.environ["HS_LIB_PATH"]).resolve()
 SOURCES = sorted((PKG / "csrc").glob("*.cu")) + sorted((PKG / "csrc").glob("*.cuh")) + sorted(
     (PKG / "csrc").glob("*.h")) + [PKG.parent / "include" / "hetsched_b200.h"]
 
@@ -42,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objdir = LIB_PATH.parent / "obj"
     objdir.mkdir(parents=True, exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + os.environ.get("HS_NVCC_EXTRA", "").split()
     cus = sorted((PKG / "csrc").glob("*.cu"))
 
     def deps(cu: Path) -> set:

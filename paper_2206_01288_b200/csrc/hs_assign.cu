@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) materialize_kernel(MaterializeArgs a, Scr
         for (int i = lane; i < km; i += kWarp) mem[i] = a.groups[p * km + i];
         __syncwarp();
         double dp, pp;
-        if (m == 8 && sizeof(KeyT) == 2 && a.nvals <= 0x8000)
+        if (m == 8 && sizeof(KeyT) == 2)
             warp_price<KeyT, true>(v, ws, mem, lane, dp, pp);
         else
             warp_price<KeyT, false>(v, ws, mem, lane, dp, pp);

@@ -228,7 +228,7 @@ static hs::EvalArgs base_args(const hs_instance* h) {
 // kernel of chunk c runs on `s` (the stage CTAs fit beside the cluster CTAs'
 // shared memory); ping-pong stage buffers, event-ordered.
 static int launch_two(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
-    const bool m8 = a.key16 && a.m == 8 && a.nvals <= 0x8000;
+    const bool m8 = a.key16 && a.m == 8;
     if (!h->two_E[set][0]) {
         for (int i = 0; i < 2; i++) {
             CK(cudaMalloc(&h->two_E[set][i], (size_t)h->two_chunk * hs::kStageStride * 8), "cudaMalloc stage graphs");
@@ -271,7 +271,7 @@ static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream
     if (h->k > hs::kWarpK && !a.order && h->two.rwords) return launch_two(h, a, set, s);
     if (h->k > hs::kWarpK)
         return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
-                                   a.key16 && a.m == 8 && a.nvals <= 0x8000, s);
+                                   a.key16 && a.m == 8, s);
     return hs::launch_eval(a, h->plan, s);
 }
 

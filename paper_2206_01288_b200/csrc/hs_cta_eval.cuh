@@ -164,14 +164,11 @@ __device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, con
         const int16_t* B = mem + j2 * m;
         uint32_t L;
         if (kM8) {
-            uint32_t K[8][4];
-#pragma unroll
-            for (int r = 0; r < 8; r++) {
+            L = match8_dp([&](int r, uint32_t(&kn)[4]) {
                 const KeyT* row = RK + (size_t)A[r] * rs;
 #pragma unroll
-                for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[B[q]] | ((uint32_t)row[B[q + 4]] << 16);
-            }
-            L = Match8::solve(K);
+                for (int q = 0; q < 4; q++) kn[q] = (uint32_t)row[B[q]] | ((uint32_t)row[B[q + 4]] << 16);
+            });
         } else {
             L = bottleneck_threshold<uint32_t>(
                 m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * rs + B[c]]; }, 0xffffffffu);

@@ -52,7 +52,10 @@ __global__ void rank_kernel(int64_t nn, const double* __restrict__ pp, const dou
 // registers): with the compact Held-Karp table (stage order wanted) and with
 // the two-layer one (no order: 4.4 KB less scratch per warp)
 constexpr int kEvalWarps = 20;
-constexpr int kEvalWarpsRoll = 28;
+#ifndef HS_EVAL_WARPS_ROLL
+#define HS_EVAL_WARPS_ROLL 24
+#endif
+constexpr int kEvalWarpsRoll = HS_EVAL_WARPS_ROLL;
 
 template <bool kSmemTables, typename KeyT, bool kM8, bool kRoll>
 __global__ void __launch_bounds__(32 * (kRoll ? kEvalWarpsRoll : kEvalWarps))
@@ -178,7 +181,7 @@ int eval_plan(const EvalArgs& a, int sm_count, size_t smem_optin, EvalPlan* plan
                  &plan->roll_smem))
         return -2;
     plan->blocks = sm_count;
-    plan->m8 = a.key16 && a.m == 8 && a.nvals <= 0x8000;
+    plan->m8 = a.key16 && a.m == 8;
     return 0;
 }
 

@@ -198,7 +198,7 @@ int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* pla
                 plan->warps = W;
                 plan->smem_tables = st;
                 plan->smem = b;
-                plan->m8 = sh.key16 && sh.m == 8 && sh.nvals <= 0x8000;
+                plan->m8 = sh.key16 && sh.m == 8;
                 plan->cta = sh.k > 8;
                 return 0;
             }

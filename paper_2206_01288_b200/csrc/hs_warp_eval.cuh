@@ -3,6 +3,7 @@
 // kernel (K3), so both produce the same bits.
 #pragma once
 #include "hs_eval.cuh"
+#include "hs_match8_dp.cuh"
 #include "hs_internal.h"
 
 namespace hs {
@@ -162,14 +163,11 @@ __device__ inline void warp_price(const EvalView<KeyT>& v, const WarpScratch& s,
             int b[8];
 #pragma unroll
             for (int c = 0; c < 8; c++) b[c] = B[c];
-            uint32_t K[8][4];
-#pragma unroll
-            for (int r = 0; r < 8; r++) {
+            L = match8_dp([&](int r, uint32_t(&kn)[4]) {
                 const KeyT* row = v.RK + (size_t)A[r] * v.rs;
 #pragma unroll
-                for (int q = 0; q < 4; q++) K[r][q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
-            }
-            L = Match8::solve(K);
+                for (int q = 0; q < 4; q++) kn[q] = (uint32_t)row[b[q]] | ((uint32_t)row[b[q + 4]] << 16);
+            });
         } else {
             L = bottleneck_threshold<uint32_t>(
                 m, [&](int r, int c) { return (uint32_t)v.RK[(size_t)A[r] * v.rs + B[c]]; }, 0xffffffffu);
