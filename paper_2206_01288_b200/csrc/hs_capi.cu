@@ -272,6 +272,7 @@ static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream
     if (h->k > hs::kWarpK)
         return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
                                    a.key16 && a.m == 8, s);
+    if (hs::eval8_applicable(a, h->smem_optin)) return hs::launch_eval8(a, h->sm_count, s);
     return hs::launch_eval(a, h->plan, s);
 }
 

@@ -1,0 +1,182 @@
+// hs_eval8.cu -- K1 for the paper shape (d_pp = 8, d_dp = 8, N = 64, u16 keys):
+// one warp prices four candidate layouts at a time (comm_cost,
+// costmodel.py:217-229), lane = (candidate c = lane / 8, slot g = lane % 8).
+//
+//   load      : lane (c, g) reads group g of candidate c -- one 16-byte
+//               vector (the quad's 512 bytes are one coalesced request);
+//               validation (costmodel.py:58-72) by shuffles in the 8 lanes.
+//   datap     : lane (c, g) forms the 8 numpy pairwise row sums of group g
+//               and their max (datap_cost_group, costmodel.py:154-168); the
+//               candidate's datap is the max over its 8 lanes.
+//   matchings : the quad's 112 group pairs over the 32 lanes (3.5 rounds),
+//               each the branch-free u16x2 subset DP (hs_match8_dp.cuh) ->
+//               bottleneck rank -> exact double (costmodel.py:200-208).
+//   Held-Karp : lane (c, u) computes every state ending at u from registers
+//               holding E[u][.] (hs_hk8_gen.cuh); pipe = min over the lanes.
+//
+// Tables staged once per persistent CTA: the Held-Karp offset rows, the u16
+// rank table and the DP table (odd row strides).  Outputs are bit-identical
+// to the schedule-driven warp kernel (hs_kernels.cu) and to the reference.
+#include "hs_hk8_gen.cuh"
+#include "hs_match8_dp.cuh"
+#include "hs_warp_eval.cuh"
+
+namespace hs {
+
+constexpr int kE8Warps = 8;
+constexpr int kE8DS = 65;  // DP row stride (doubles)
+constexpr int kE8RS = 66;  // rank row stride (u16): 33 words, odd
+constexpr size_t kE8OffBytes = (size_t)8 * kHK8Words * 4 + 64;  // + layer-2 edge slots
+constexpr size_t kE8RkBytes = ((size_t)64 * kE8RS * 2 + 15) & ~(size_t)15;
+constexpr size_t kE8DpBytes = (size_t)64 * kE8DS * 8;
+constexpr size_t kE8WarpBytes = (size_t)4 * kHK8Block * 8 + 4 * 64 * 2;
+constexpr size_t kE8Smem = kE8OffBytes + kE8RkBytes + kE8DpBytes + kE8Warps * kE8WarpBytes;
+
+__device__ __forceinline__ double shfl_xor_d(double x, int m) {
+    return __longlong_as_double(__shfl_xor_sync(0xffffffffu, __double_as_longlong(x), m));
+}
+
+__device__ __forceinline__ int i16(uint32_t w, int hi) { return hi ? (int)(int16_t)(w >> 16) : (int)(int16_t)(w & 0xFFFFu); }
+
+template <bool kPerGroup>
+__global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem);
+    uint16_t* rk = reinterpret_cast<uint16_t*>(smem + kE8OffBytes);
+    double* dp = reinterpret_cast<double*>(smem + kE8OffBytes + kE8RkBytes);
+    unsigned char* wsm = smem + kE8OffBytes + kE8RkBytes + kE8DpBytes;
+    const uint16_t* grk = reinterpret_cast<const uint16_t*>(a.rank);
+    uint16_t* eslot = reinterpret_cast<uint16_t*>(offs + 8 * kHK8Words);
+    for (int i = threadIdx.x; i < 8 * kHK8Words; i += blockDim.x) offs[i] = kHK8Offs[i];
+    if (threadIdx.x < 28) eslot[threadIdx.x] = kHK8Edge[threadIdx.x];
+    for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+        const int r = i >> 6, c = i & 63;
+        rk[r * kE8RS + c] = grk[i];
+        dp[r * kE8DS + c] = a.dp[i];
+    }
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int c = lane >> 3, g = lane & 7;
+    char* blocks = reinterpret_cast<char*>(wsm + (size_t)wid * kE8WarpBytes);
+    char* blk = blocks + (size_t)c * kHK8Block * 8;
+    int16_t* memw = reinterpret_cast<int16_t*>(blocks + (size_t)4 * kHK8Block * 8);
+    const uint4* t4 = reinterpret_cast<const uint4*>(offs + g * kHK8Words);
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    const uint4* gsrc = reinterpret_cast<const uint4*>(a.groups);
+    const uint4 ident = make_uint4((uint32_t)(8 * g) | (uint32_t)(8 * g + 1) << 16,
+                                   (uint32_t)(8 * g + 2) | (uint32_t)(8 * g + 3) << 16,
+                                   (uint32_t)(8 * g + 4) | (uint32_t)(8 * g + 5) << 16,
+                                   (uint32_t)(8 * g + 6) | (uint32_t)(8 * g + 7) << 16);
+
+    for (int64_t q = (int64_t)blockIdx.x * W + wid; q * 4 < a.P; q += (int64_t)gridDim.x * W) {
+        const int64_t p = q * 4 + c;
+        const bool live = p < a.P;
+        uint4 gm = live ? __ldg(gsrc + p * 8 + g) : ident;
+        // validation: in range, ascending, the candidate's 8 groups cover 0..63
+        int mem[8];
+        mem[0] = i16(gm.x, 0), mem[1] = i16(gm.x, 1), mem[2] = i16(gm.y, 0), mem[3] = i16(gm.y, 1);
+        mem[4] = i16(gm.z, 0), mem[5] = i16(gm.z, 1), mem[6] = i16(gm.w, 0), mem[7] = i16(gm.w, 1);
+        bool ok = true;
+        uint64_t cover = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            ok = ok && mem[i] >= 0 && mem[i] < 64 && (i == 0 || mem[i - 1] < mem[i]);
+            cover |= 1ull << (mem[i] & 63);
+        }
+        uint32_t cl = (uint32_t)cover, ch = (uint32_t)(cover >> 32), okb = ok;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) {
+            cl |= __shfl_xor_sync(0xffffffffu, cl, m);
+            ch |= __shfl_xor_sync(0xffffffffu, ch, m);
+            okb &= __shfl_xor_sync(0xffffffffu, okb, m);
+        }
+        const bool bad = live && !(okb && cl == 0xffffffffu && ch == 0xffffffffu);
+        if (bad) {  // price a valid stand-in, report NaN
+            gm = ident;
+#pragma unroll
+            for (int i = 0; i < 8; i++) mem[i] = 8 * g + i;
+        }
+        reinterpret_cast<uint4*>(memw)[lane] = gm;
+        // data-parallel level: numpy pairwise row sums (the 0.0 diagonal in
+        // its slot), max over the group's rows
+        double pg = 0.0;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const double* row = dp + mem[r] * kE8DS;
+            const double s = ((row[mem[0]] + row[mem[1]]) + (row[mem[2]] + row[mem[3]])) +
+                             ((row[mem[4]] + row[mem[5]]) + (row[mem[6]] + row[mem[7]]));
+            pg = r == 0 ? s : dmax(pg, s);
+        }
+        double datap = pg;
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) datap = dmax(datap, shfl_xor_d(datap, m));
+        __syncwarp();
+        // pipeline edges: 4 x 28 group pairs over 32 lanes
+#pragma unroll 1
+        for (int t = lane; t < 112; t += 32) {
+            const int cc = t / 28, pi = t - cc * 28;
+            int j, j2;
+            decode_pair(pi, 8, j, j2);
+            const uint4 A4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j];
+            const uint4 B4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j2];
+            const uint32_t Aw[4] = {A4.x, A4.y, A4.z, A4.w};
+            const uint32_t Bw[4] = {B4.x, B4.y, B4.z, B4.w};
+            int b[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) b[i] = i16(Bw[i >> 1], i & 1);
+            const uint32_t L = match8_dp([&](int r, uint32_t(&kn)[4]) {
+                const uint16_t* row = rk + i16(Aw[r >> 1], r & 1) * kE8RS;
+#pragma unroll
+                for (int qq = 0; qq < 4; qq++) kn[qq] = (uint32_t)row[b[qq]] | ((uint32_t)row[b[qq + 4]] << 16);
+            });
+            const double e = __ldg(a.vals + L);
+            double* dst = reinterpret_cast<double*>(blocks) + cc * kHK8Block + eslot[pi];
+            dst[0] = e;  // h[{j, j2}][j] and h[{j, j2}][j2]
+            dst[kHK8EdgeStride] = e;
+        }
+        __syncwarp();
+        double pipe = hk8_lane(blk, t4);
+#pragma unroll
+        for (int m = 1; m < 8; m <<= 1) pipe = dmin(pipe, shfl_xor_d(pipe, m));
+        if (live) {
+            if (g == 0) {
+                if (bad) {
+                    a.total[p] = nan;
+                    if (a.datap) a.datap[p] = nan;
+                    if (a.pipe) a.pipe[p] = nan;
+                    atomicAdd(a.invalid, 1);
+                } else {
+                    a.total[p] = datap + pipe;
+                    if (a.datap) a.datap[p] = datap;
+                    if (a.pipe) a.pipe[p] = pipe;
+                }
+            }
+            if (kPerGroup && !bad) a.per_group[p * 8 + g] = pg;
+        }
+        __syncwarp();
+    }
+}
+
+bool eval8_applicable(const EvalArgs& a, size_t smem_optin) {
+    // 16-byte group loads: the layout array must be 16-byte aligned (views at
+    // odd offsets take the schedule-driven kernel)
+    return a.k == 8 && a.m == 8 && a.n == 64 && a.key16 && !a.order && kE8Smem <= smem_optin &&
+           ((uintptr_t)a.groups & 15) == 0;
+}
+
+int launch_eval8(const EvalArgs& a, int sm_count, cudaStream_t s) {
+    if (a.P == 0) return 0;
+    const int64_t quads = (a.P + 3) / 4;
+    const int blocks = (int)std::min<int64_t>(sm_count, (quads + kE8Warps - 1) / kE8Warps);
+    if (a.per_group) {
+        cudaFuncSetAttribute(eval8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
+        eval8_kernel<true><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(eval8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
+        eval8_kernel<false><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+}  // namespace hs
