@@ -13,7 +13,6 @@ scaling, no data-path collective); time is the max over ranks.
 from __future__ import annotations
 
 import argparse
-import contextlib
 import json
 import os
 import statistics
@@ -27,10 +26,13 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
-# rank 0 prints exactly one JSON line on stdout: NCCL's own messages (its
-# version banner included) go to stderr
-os.environ.setdefault("NCCL_DEBUG", "WARN")
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# rank 0 prints exactly one JSON line on stdout.  The ours arm moves fd 1 to
+# stderr for its whole run (JSON_FD keeps the real stdout), so NCCL's banner
+# and its communicator-init INFO lines (printed on stdout) land on stderr; a
+# caller's NCCL_DEBUG / NCCL_DEBUG_SUBSYS win
+os.environ.setdefault("NCCL_DEBUG", "INFO")
+os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+JSON_FD = 1
 
 METRIC = "layout cost-evals/sec (N=64, D_PP=8xD_DP=8)"
 WORKLOAD = ("paper setting: 64 devices, D_PP=8 x D_DP=8, GPT3-XL tasklets "
@@ -117,19 +119,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-@contextlib.contextmanager
 def stdout_to_stderr():
-    """fd-level: NCCL prints its version banner with printf at communicator
-    init, whatever NCCL_DEBUG_FILE says; keep rank 0's stdout one JSON line."""
+    """fd-level: from here on anything written to fd 1 (NCCL's printf
+    logging included) goes to stderr; emit() writes to the saved stdout."""
+    global JSON_FD
     sys.stdout.flush()
-    saved = os.dup(1)
+    JSON_FD = os.dup(1)
     os.dup2(2, 1)
-    try:
-        yield
-    finally:
-        sys.stdout.flush()
-        os.dup2(saved, 1)
-        os.close(saved)
+
+
+def emit(line: dict) -> None:
+    os.write(JSON_FD, (json.dumps(line) + "\n").encode())
 
 
 def dist_env():
@@ -142,6 +142,19 @@ def dist_env():
 def instance():
     from paper_2206_01288_b200 import PAPER_WORKLOAD, scenario_case
     return scenario_case(ARGS.case).graph(), PAPER_WORKLOAD
+
+
+def ga_instances():
+    """The GA time-to-converge anchors of tests/golden/evolve_1000.json:
+    the five paper scenarios at 8x8 and BASELINE config 1 (8 devices, 2x4,
+    case-1 links on two nodes of four, GPT3-XL at d_pp=2)."""
+    from paper_2206_01288_b200 import PAPER_WORKLOAD, scenario_case
+    from paper_2206_01288_b200.netmodel import scenario_from_ms_gbps
+    from paper_2206_01288_b200.workload import WorkloadSpec
+    out = {f"case{c}": (scenario_case(c).graph(), PAPER_WORKLOAD) for c in range(1, 6)}
+    out["config1"] = (scenario_from_ms_gbps([(4, 0.1, 100), (4, 0.1, 100)], 0.25, 25, 0).graph(),
+                      WorkloadSpec(2, 4, 2_147_483_648, 1_207_959_552))
+    return out
 
 
 def cpu_oracle_rate(g, w, seconds: float, threads: int):
@@ -162,6 +175,16 @@ def cpu_oracle_rate(g, w, seconds: float, threads: int):
     return count / dt, count, dt
 
 
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" x {os.cpu_count()} logical CPUs"
+    except OSError:
+        pass
+    return f"unknown x {os.cpu_count()}"
+
+
 def run_reference():
     rank, world, _ = dist_env()
     if rank != 0:
@@ -180,11 +203,12 @@ def run_reference():
     value = total / secs
     sample = f"{total} random 8x8 case-{ARGS.case} layouts over {ARGS.steps} steps, C oracle port of comm_cost"
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": max(world, ARGS.gpus),
         "steps": ARGS.steps, "warmup": ARGS.warmup, "ms_per_step": 1000 * secs / ARGS.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic random balanced layouts", "config": {"workload": WORKLOAD},
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -198,9 +222,8 @@ def run_ours():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        with stdout_to_stderr():
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-            dist.barrier()
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.barrier()
     dev = torch.device(f"cuda:{local}")
     g, w = instance()
     inst = N.instance_for(g, w, local)
@@ -323,9 +346,13 @@ def run_ours():
         from oracle import oracle as O
         threads = O.cpu_count()
         rate, count, dt = cpu_oracle_rate(g, w, ARGS.cpu_seconds, threads)
+        rate1, count1, dt1 = cpu_oracle_rate(g, w, min(3.0, ARGS.cpu_seconds), 1)
         line["cpu_baseline"] = {"value": rate, "unit": "evals/s", "cores": threads, "kind": "port",
                                 "sample": f"{count} random 8x8 case-{ARGS.case} layouts in {dt:.1f} s "
-                                          f"(C oracle restatement of comm_cost, {threads} threads)"}
+                                          f"(C oracle restatement of comm_cost, {threads} threads)",
+                                "one_core": {"value": rate1, "sample": f"{count1} layouts in {dt1:.1f} s, 1 thread"},
+                                "cpu_model": cpu_model(),
+                                "python_reference_per_core_build_container": "179-292 evals/s (SURVEY.md §8(d))"}
         if "ga" in line:
             # the same 1000-generation evolve through the C oracle port on one
             # host core (the GA is one sequential chain of generations)
@@ -337,7 +364,7 @@ def run_ours():
                 "seconds": t_cpu, "cores": 1, "kind": "port",
                 "same_best_total": bool(float(ref["total"]) == line["ga"]["time_to_converge"]["best_total_s"])}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 
@@ -350,29 +377,41 @@ def ga_legs(g, w, rank, world, local, barrier, dist):
     from paper_2206_01288_b200 import scheduler as S
 
     out = {}
-    cfg = S.ScheduleConfig(pop_size=64, generations=1000, local_search="ours", seed=0)
-    barrier()
-    t0 = time.perf_counter()
-    res = S.evolve(g, w, cfg)
-    torch.cuda.synchronize()
-    t_ga = time.perf_counter() - t0
-    best = [b for _, b, _ in res.trace]
-    conv = max([0] + [i for i in range(1, len(best)) if best[i] < best[i - 1]])
     gold_path = ROOT / "tests" / "golden" / "evolve_1000.json"
-    ident, ref_s = None, None
-    if gold_path.exists() and ARGS.case == 5:
-        run = next(r for r in json.loads(gold_path.read_text())["runs"] if r["inst"] == "case5")
-        ref_s = run["wall_s"]
-        ident = (res.evaluations == run["evaluations"]
-                 and [b for _, b, _ in res.trace] == [float.fromhex(x) for x in run["trace_best"]]
-                 and [m for _, _, m in res.trace] == [float.fromhex(x) for x in run["trace_mean"]]
-                 and [list(x) for x in res.best_partition.key()] == run["partition"])
+    gold = {r["inst"]: r for r in json.loads(gold_path.read_text())["runs"]} if gold_path.exists() else {}
+    per_case = {}
+    for name, (gi, wi) in ga_instances().items():
+        cfg = S.ScheduleConfig(pop_size=64, generations=1000, local_search="ours", seed=0)
+        S.evolve(gi, wi, S.ScheduleConfig(pop_size=64, generations=2, local_search="ours", seed=0))  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        res = S.evolve(gi, wi, cfg)
+        torch.cuda.synchronize()
+        t_ga = time.perf_counter() - t0
+        best = [b for _, b, _ in res.trace]
+        conv = max([0] + [i for i in range(1, len(best)) if best[i] < best[i - 1]])
+        run = gold.get(name)
+        ident = None
+        if run is not None:
+            ident = (res.evaluations == run["evaluations"]
+                     and best == [float.fromhex(x) for x in run["trace_best"]]
+                     and [m for _, _, m in res.trace] == [float.fromhex(x) for x in run["trace_mean"]]
+                     and [list(x) for x in res.best_partition.key()] == run["partition"])
+        per_case[name] = {"seconds": t_ga, "last_improving_generation": conv,
+                          "seconds_to_last_improvement": t_ga * (conv + 1) / len(best),
+                          "best_total_s": res.best_cost.total, "evaluations": res.evaluations,
+                          "identical_to_reference": ident,
+                          "reference_python_seconds_build_container": run["wall_s"] if run else None}
+    head = per_case[f"case{ARGS.case}"]
     out["time_to_converge"] = {
         "workload": f"evolve(pop=64, generations=1000, local_search='ours', seed=0), case {ARGS.case}",
-        "seconds": t_ga, "generations": len(res.trace), "last_improving_generation": conv,
-        "best_total_s": res.best_cost.total, "evaluations": res.evaluations,
-        "identical_to_reference": ident,
-        "reference_python_seconds_build_container": ref_s,
+        "seconds": head["seconds"], "generations": 1000,
+        "last_improving_generation": head["last_improving_generation"],
+        "best_total_s": head["best_total_s"], "evaluations": head["evaluations"],
+        "identical_to_reference": head["identical_to_reference"],
+        "reference_python_seconds_build_container": head["reference_python_seconds_build_container"],
+        "per_case": per_case,
+        "timed": "wall clock around evolve() incl. the final result download, after a 2-generation warm-up",
     }
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     I = ARGS.islands or sms * 8
@@ -491,9 +530,26 @@ def sweep_legs(local):
     return out
 
 
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this script as N ranks
+    (one process per GPU, NCCL) through torch.distributed.run on this node;
+    rank 0's JSON line is this process's stdout."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
 if __name__ == "__main__":
     ARGS = parse()
+    if ARGS.gpus > 1 and "WORLD_SIZE" not in os.environ and ARGS.impl == "ours":
+        sys.exit(self_launch(ARGS.gpus))
     if ARGS.impl == "reference":
         run_reference()
     else:
+        stdout_to_stderr()
         run_ours()

@@ -121,7 +121,10 @@ int hs_ga_import(hs_ga *ga, int elites, const int16_t *groups, const double *cos
  * host buffers: best_groups [islands][k*m], best3 [islands][3] (total, datap,
  * pipelinep), best_per_group [islands][k], best_order [islands][k],
  * trace_best / trace_mean [islands][generations], trace_len [islands],
- * evaluations [islands], rng [islands] (advanced states).  NULL skips. */
+ * evaluations [islands], rng [islands] (advanced states).  NULL skips.
+ * Synchronizes the stream of the session's latest run / export / import
+ * first; returns -2 if an island is neither stopped (patience) nor run to
+ * `generations` (call hs_ga_run(ga, generations, ...) first). */
 int hs_ga_result(hs_ga *ga, int16_t *best_groups, double *best3, double *best_per_group, int8_t *best_order,
                  double *trace_best, double *trace_mean, int32_t *trace_len, int64_t *evaluations, hs_pcg64 *rng);
 int hs_ga_destroy(hs_ga *ga);

@@ -114,8 +114,23 @@ def _check_partition(p, g, w) -> None:
             f"partition shape {len(p.groups)}x{len(p.groups[0])} does not match workload {w.d_pp}x{w.d_dp}")
 
 
+def shard_bounds(P: int, G: int) -> list[tuple[int, int]]:
+    """Contiguous split of P candidates over G devices:
+    the first P % G shards hold one extra candidate; empty shards are kept
+    so shard i always belongs to device i."""
+    if G < 1:
+        raise ValueError("need at least one device")
+    base, extra = divmod(int(P), G)
+    out, lo = [], 0
+    for i in range(G):
+        hi = lo + base + (1 if i < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
 def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = False, device: int | None = None,
-                    heuristic: bool = False):
+                    heuristic: bool = False, devices=None):
     """Costs of a batch of partitions in one GPU pass.
 
     ``groups``: int16-compatible [P, d_pp, d_dp] with ascending members --
@@ -124,8 +139,19 @@ def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = Fals
     Returns a dict of arrays (numpy for host input, torch for device input):
     total, datap, pipelinep and optionally per_group [P, d_pp], order [P, d_pp].
     Malformed partitions raise CostModelError.
+
+    ``devices=[d0, d1, ...]`` splits the population contiguously over those
+    GPUs (shard_bounds), each pricing its slice against its own replica of
+    the pair tables, concurrently; results are gathered back in input order
+    (numpy for host input, a tensor on the input's device otherwise).  This
+    is the batch seam the reference parallelises with ``threads``
+    (scheduler.py:537-542), bit-identical to one device.
     """
     validate_workload(w, g.lat.shape[0])
+    if devices is not None and len(devices) > 1:
+        return _comm_cost_batch_multi(g, groups, w, per_group, order, heuristic, [int(d) for d in devices])
+    if devices is not None and len(devices) == 1:
+        device = int(devices[0])
     if w.d_pp > 16:
         if not heuristic:
             raise ValueError(f"exact path search is limited to 16 vertices, got {w.d_pp}; "
@@ -138,16 +164,8 @@ def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = Fals
         if a.ndim != 3 or a.shape[1:] != (inst.k, inst.m):
             raise CostModelError(f"expected groups of shape [P, {inst.k}, {inst.m}], got {a.shape}")
         P = a.shape[0]
-        out = {"total": np.empty(P), "datap": np.empty(P), "pipelinep": np.empty(P)}
-        if per_group:
-            out["per_group"] = np.empty((P, k))
-        if order:
-            out["order"] = np.empty((P, k), dtype=np.int8)
-        bad = np.zeros(1, dtype=np.int32)
-        N.check(N.lib().hs_eval_batch_host(inst.handle, a.ctypes.data, P, N.ptr(out["total"]), N.ptr(out["datap"]),
-                                           N.ptr(out["pipelinep"]), N.ptr(out.get("per_group")),
-                                           N.ptr(out.get("order")), bad.ctypes.data), "hs_eval_batch_host")
-        nbad = int(bad[0])
+        out = _host_outputs(P, k, per_group, order)
+        nbad = _eval_host_into(inst, a, out)
     else:
         torch = N.torch_cuda()
         t = groups
@@ -156,22 +174,102 @@ def comm_cost_batch(g, groups, w, *, per_group: bool = False, order: bool = Fals
         if t.dim() != 3 or tuple(t.shape[1:]) != (inst.k, inst.m):
             raise CostModelError(f"expected groups of shape [P, {inst.k}, {inst.m}], got {tuple(t.shape)}")
         P = t.shape[0]
-        dev = f"cuda:{inst.device}"
-        out = {name: torch.empty(P, dtype=torch.float64, device=dev) for name in ("total", "datap", "pipelinep")}
-        if per_group:
-            out["per_group"] = torch.empty((P, k), dtype=torch.float64, device=dev)
-        if order:
-            out["order"] = torch.empty((P, k), dtype=torch.int8, device=dev)
-        bad = torch.zeros(1, dtype=torch.int32, device=dev)
-        N.check(N.lib().hs_eval_batch(inst.handle, t.data_ptr(), P, out["total"].data_ptr(), out["datap"].data_ptr(),
-                                      out["pipelinep"].data_ptr(), N.ptr(out.get("per_group")),
-                                      N.ptr(out.get("order")), bad.data_ptr(), N.stream_ptr(inst.device)),
-                "hs_eval_batch")
+        out, bad = _launch_device(inst, t, per_group, order)
         nbad = int(bad.item())
     if nbad:
         raise CostModelError(
             f"{nbad} of {P} partitions are not balanced partitions of 0..N-1 with ascending members")
     return out
+
+
+def _launch_device(inst, t, per_group: bool, order: bool):
+    """hs_eval_batch on the device's current stream (no synchronisation):
+    returns the output tensors and the device-side malformed-row counter."""
+    torch = N.torch_cuda()
+    P, k = t.shape[0], inst.k
+    dev = f"cuda:{inst.device}"
+    out = {name: torch.empty(P, dtype=torch.float64, device=dev) for name in ("total", "datap", "pipelinep")}
+    if per_group:
+        out["per_group"] = torch.empty((P, k), dtype=torch.float64, device=dev)
+    if order:
+        out["order"] = torch.empty((P, k), dtype=torch.int8, device=dev)
+    bad = torch.zeros(1, dtype=torch.int32, device=dev)
+    N.check(N.lib().hs_eval_batch(inst.handle, t.data_ptr(), P, out["total"].data_ptr(), out["datap"].data_ptr(),
+                                  out["pipelinep"].data_ptr(), N.ptr(out.get("per_group")), N.ptr(out.get("order")),
+                                  bad.data_ptr(), N.stream_ptr(inst.device)), "hs_eval_batch")
+    return out, bad
+
+
+def _host_outputs(P: int, k: int, per_group: bool, order: bool) -> dict:
+    out = {"total": np.empty(P), "datap": np.empty(P), "pipelinep": np.empty(P)}
+    if per_group:
+        out["per_group"] = np.empty((P, k))
+    if order:
+        out["order"] = np.empty((P, k), dtype=np.int8)
+    return out
+
+
+def _eval_host_into(inst, a: np.ndarray, out: dict) -> int:
+    """hs_eval_batch_host over contiguous host rows ``a`` into the (views
+    of) output arrays ``out``; returns the malformed-row count."""
+    bad = np.zeros(1, dtype=np.int32)
+    N.check(N.lib().hs_eval_batch_host(inst.handle, a.ctypes.data, a.shape[0], N.ptr(out["total"]),
+                                       N.ptr(out["datap"]), N.ptr(out["pipelinep"]), N.ptr(out.get("per_group")),
+                                       N.ptr(out.get("order")), bad.ctypes.data), "hs_eval_batch_host")
+    return int(bad[0])
+
+
+def _comm_cost_batch_multi(g, groups, w, per_group, order, heuristic, devices):
+    """comm_cost_batch over several GPUs: contiguous shards, one replica of
+    the pair tables per device, all devices busy at once (host input: one
+    host thread per device in the synchronous host-buffer entry, which
+    releases the GIL; device input: per-device async launches on each
+    device's current stream)."""
+    if w.d_pp > 16:
+        if not heuristic:
+            raise ValueError(f"exact path search is limited to 16 vertices, got {w.d_pp}; "
+                             "pass heuristic=True to accept an approximate tour")
+    k, m = w.d_pp, w.d_dp
+    host = isinstance(groups, np.ndarray) or not hasattr(groups, "data_ptr")
+    shape = tuple(groups.shape) if not host else np.shape(groups)
+    if len(shape) != 3 or tuple(shape[1:]) != (k, m):
+        raise CostModelError(f"expected groups of shape [P, {k}, {m}], got {tuple(shape)}")
+    P = shape[0]
+    bounds = shard_bounds(P, len(devices))
+    if host:
+        a = np.ascontiguousarray(groups, dtype=np.int16)
+        if w.d_pp > 16:  # the heuristic path returns fresh arrays per shard
+            parts = [comm_cost_batch(g, a[lo:hi], w, per_group=per_group, order=order, device=d, heuristic=True)
+                     for d, (lo, hi) in zip(devices, bounds)]
+            return {key: np.concatenate([p[key] for p in parts]) for key in parts[0]}
+        out = _host_outputs(P, k, per_group, order)
+        insts = [N.instance_for(g, w, d) for d in devices]  # tables built up front, in order
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=len(devices)) as ex:
+            futs = [ex.submit(_eval_host_into, inst, a[lo:hi], {key: val[lo:hi] for key, val in out.items()})
+                    for inst, (lo, hi) in zip(insts, bounds) if hi > lo]
+            nbad = sum(f.result() for f in futs)
+        if nbad:
+            raise CostModelError(
+                f"{nbad} of {P} partitions are not balanced partitions of 0..N-1 with ascending members")
+        return out
+    torch = N.torch_cuda()
+    src = groups.device
+    if w.d_pp > 16:
+        parts = [comm_cost_batch(g, groups[lo:hi].cpu().numpy(), w, per_group=per_group, order=order, device=d,
+                                 heuristic=True) for d, (lo, hi) in zip(devices, bounds)]
+        return {key: torch.from_numpy(np.concatenate([p[key] for p in parts])).to(src) for key in parts[0]}
+    shards = []
+    for d, (lo, hi) in zip(devices, bounds):  # launch every shard before any synchronisation
+        inst = N.instance_for(g, w, d)
+        with torch.cuda.device(d):
+            t = groups[lo:hi].to(device=f"cuda:{d}", dtype=torch.int16).contiguous()
+            shards.append(_launch_device(inst, t, per_group, order))
+    nbad = sum(int(bad.item()) for _, bad in shards)
+    if nbad:
+        raise CostModelError(
+            f"{nbad} of {P} partitions are not balanced partitions of 0..N-1 with ascending members")
+    return {key: torch.cat([out[key].to(src) for out, _ in shards]) for key in shards[0][0]}
 
 
 def _comm_cost_batch_heuristic(g, groups, w, per_group, order, device):
@@ -218,8 +316,12 @@ def comm_cost(g, p, w, heuristic: bool = False) -> CostBreakdown:
 def datap_cost(g, p, w) -> tuple[float, tuple[float, ...]]:
     """Data-parallel level: slowest group and the per-group values."""
     _check_partition(p, g, w)
-    cb = comm_cost(g, p, w)
-    return cb.datap, cb.per_group_datap
+    validate_workload(w, g.lat.shape[0])
+    if w.d_dp == 1:
+        per = tuple(0.0 for _ in p.groups)
+    else:  # the data-parallel level only: no Held-Karp, any d_pp (costmodel.py:171-175)
+        per = tuple(float(x) for x in datap_cost_groups(g, np.asarray(p.groups), w))
+    return max(per), per
 
 
 def datap_cost_group(g, group: Iterable[int], w) -> float:

@@ -65,6 +65,7 @@ struct hs_ga {
     int16_t* out_groups = nullptr;
     double* hk_scratch = nullptr;
     long long* prof = nullptr;  // HS_GA_PROFILE=1: driver-phase cycle counters of island 0
+    cudaStream_t last = nullptr;  // stream of the latest run / export / import (hs_ga_result syncs it)
 };
 
 static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
@@ -160,6 +161,7 @@ int hs_ga_run(hs_ga* ga, int until, void* stream) {
     hs::GAArgs a = ga_args(ga, until, until >= ga->cfg.generations);
     if (hs::launch_ga(a, ga->plan, ga->islands, ga->h->rank16 != nullptr, (cudaStream_t)stream))
         return fail(-1, "ga launch", cudaGetLastError());
+    ga->last = (cudaStream_t)stream;
     return 0;
 }
 
@@ -170,6 +172,7 @@ int hs_ga_export(hs_ga* ga, int elites, int16_t* groups, double* costs, void* st
     if (hs::launch_export(ga->islands, ga->cfg.pop_size, ga->h->k * ga->h->m, elites, ga->pop, ga->cost, groups, costs,
                           (cudaStream_t)stream))
         return fail(-1, "export launch", cudaGetLastError());
+    ga->last = (cudaStream_t)stream;
     return 0;
 }
 
@@ -180,6 +183,7 @@ int hs_ga_import(hs_ga* ga, int elites, const int16_t* groups, const double* cos
     if (hs::launch_import(ga->islands, ga->cfg.pop_size, ga->h->k * ga->h->m, elites, ga->pop, ga->cost, ga->best,
                           ga->state, groups, costs, src, (cudaStream_t)stream))
         return fail(-1, "import launch", cudaGetLastError());
+    ga->last = (cudaStream_t)stream;
     return 0;
 }
 
@@ -187,17 +191,26 @@ int hs_ga_result(hs_ga* ga, int16_t* best_groups, double* best3, double* best_pe
                  double* trace_best, double* trace_mean, int32_t* trace_len, int64_t* evaluations, hs_pcg64* rng) {
     if (!ga) return fail(-2, "null handle");
     DeviceGuard dg(ga->h->device);
-    // a run stopped by patience before `generations` still needs finalizing
-    hs::GAArgs a = ga_args(ga, ga->cfg.generations, 1);
+    // the session's work may still be in flight on the caller's (possibly
+    // non-blocking) stream: drain it before reading the island states
+    CK(cudaStreamSynchronize(ga->last), "ga sync");
     std::vector<hs::GAState> st(ga->islands);
     CK(cudaMemcpy(st.data(), ga->state, sizeof(hs::GAState) * ga->islands, cudaMemcpyDeviceToHost), "download state");
     bool need = false;
-    for (auto& x : st) need |= !x.finalized;
+    for (auto& x : st) {
+        if (!x.stopped && x.gen < ga->cfg.generations)
+            return fail(-2, "GA session not finished: run it to `generations` (hs_ga_run) before reading results");
+        need |= !x.finalized;
+    }
     if (need) {
-        if (hs::launch_ga(a, ga->plan, ga->islands, ga->h->rank16 != nullptr, 0)) return fail(-1, "ga finalize");
+        // islands stopped by patience before `generations` still price their
+        // canonical best; no island runs further generations
+        hs::GAArgs a = ga_args(ga, ga->cfg.generations, 1);
+        if (hs::launch_ga(a, ga->plan, ga->islands, ga->h->rank16 != nullptr, ga->last))
+            return fail(-1, "ga finalize", cudaGetLastError());
+        CK(cudaStreamSynchronize(ga->last), "ga sync");
         CK(cudaMemcpy(st.data(), ga->state, sizeof(hs::GAState) * ga->islands, cudaMemcpyDeviceToHost), "download");
     }
-    CK(cudaDeviceSynchronize(), "ga sync");
     const int I = ga->islands, k = ga->h->k, km = k * ga->h->m, G = ga->cfg.generations;
     if (best_groups) CK(cudaMemcpy(best_groups, ga->out_groups, (size_t)I * km * 2, cudaMemcpyDeviceToHost), "D2H");
     if (best3) CK(cudaMemcpy(best3, ga->out3, (size_t)I * 3 * 8, cudaMemcpyDeviceToHost), "D2H");

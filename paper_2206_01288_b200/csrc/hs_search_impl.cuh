@@ -1005,7 +1005,7 @@ static __device__ bool chain_round8(LS& s, ChainRegs& c, RoundCache& rc, int lan
     // against the home costs published in shared memory
     double* hs = s.home;  // n doubles, otherwise unused on this path
     if (row < 0) {
-        hs[lane] = c.h0;
+        if (lane < s.n) hs[lane] = c.h0;
         if (lane + 32 < s.n) hs[lane + 32] = c.h1;
         __syncwarp();
     }

@@ -85,3 +85,22 @@ def test_no_cpu_fallback_without_gpu():
     from tests._instances import g4
     with pytest.raises(N.NativeUnavailable):
         hs.comm_cost(g4(), hs.Partition(((0, 1), (2, 3))), hs.WorkloadSpec(2, 2, 1.25e8, 5e8))
+
+
+def test_batch_assignment_apis_validate_on_host():
+    """Malformed rows are rejected before any device call (the kernels index
+    the pair tables by these ids)."""
+    import numpy as np
+
+    from paper_2206_01288_b200 import PAPER_WORKLOAD, AssignmentError, scenario_case
+    from paper_2206_01288_b200.evaluation import evaluate_assignments, materialize_batch
+    g = scenario_case(5).graph()
+    good = np.arange(64, dtype=np.int16).reshape(1, 8, 8)
+    for bad in (good + 1, np.where(good == 5, 4, good), good[:, ::-1, ::-1].copy()):
+        with pytest.raises(AssignmentError):
+            materialize_batch(g, bad, PAPER_WORKLOAD)
+    with pytest.raises(AssignmentError):
+        materialize_batch(g, good.reshape(1, 4, 16), PAPER_WORKLOAD)
+    grid = np.arange(64, dtype=np.int16).reshape(1, 8, 8)
+    with pytest.raises(AssignmentError, match="1 of 2 grids"):
+        evaluate_assignments(g, np.concatenate([grid, np.minimum(grid, 62)]), PAPER_WORKLOAD)

@@ -74,3 +74,21 @@ def test_datap_cost_group_golden():
         hs.datap_cost_group(g, [0, 0, 1, 2, 3, 4, 5, 6], w)
     with pytest.raises(hs.CostModelError, match="does not match d_dp"):
         hs.datap_cost_group(g, [0, 1], w)
+
+
+@pytest.mark.parametrize("name", ["case5", "config1", "r10_10x1", "config5"])
+def test_datap_cost_is_the_data_parallel_level_only(name):
+    """datap_cost == comm_cost's datap / per_group where exact pricing exists,
+    and needs no Held-Karp (works for any d_pp, like costmodel.py:171-175)."""
+    from oracle import oracle as O
+    g, w = I.instance(name)
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        p = hs.random_partition(rng, g.lat.shape[0], w.d_pp, w.d_dp)
+        mx, per = hs.datap_cost(g, p, w)
+        if w.d_pp <= 16:
+            cb = hs.comm_cost(g, p, w)
+            assert mx == cb.datap and per == cb.per_group_datap
+        _, d, _ = O.Oracle.of(g, w).comm_cost_batch(np.asarray([p.groups], dtype=np.int16)) if w.d_pp <= 16 \
+            else (None, [mx], None)
+        assert mx == d[0] and mx == max(per)

@@ -282,3 +282,36 @@ def test_cluster_held_karp_device_batch_with_malformed_rows():
     r = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w)
     t, d, p = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
     assert np.array_equal(r["total"].cpu().numpy(), t)
+
+
+def _devices_for_split():
+    import torch
+    n = torch.cuda.device_count()
+    return list(range(n)) if n > 1 else [0, 0]
+
+
+@pytest.mark.parametrize("name", ["case5", "config4"])
+def test_multi_device_split_is_bitwise_single_device(name):
+    """comm_cost_batch(devices=[...]) shards contiguously over GPUs (or two
+    host threads on one GPU) and must equal the single-device result."""
+    g, w = I.instance(name)
+    P = 20_001 if w.d_pp <= 8 else 301
+    parts = _random_parts(21, P, g.lat.shape[0], w.d_pp, w.d_dp)
+    one = hs.comm_cost_batch(g, parts, w, per_group=True)
+    devs = _devices_for_split()
+    many = hs.comm_cost_batch(g, parts, w, per_group=True, devices=devs)
+    for key in one:
+        assert np.array_equal(one[key], many[key]), key
+
+
+def test_multi_device_split_device_tensor_and_errors():
+    import torch
+    g, w = I.instance("case3")
+    parts = _random_parts(22, 5003, 64, 8, 8)
+    ref = hs.comm_cost_batch(g, parts, w)["total"]
+    got = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w, devices=_devices_for_split())["total"]
+    assert got.device.type == "cuda" and np.array_equal(got.cpu().numpy(), ref)
+    bad = parts.copy()
+    bad[-1, 0, 0] = bad[-1, 0, 1]
+    with pytest.raises(hs.CostModelError, match="1 of 5003"):
+        hs.comm_cost_batch(g, bad, w, devices=_devices_for_split())

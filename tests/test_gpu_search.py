@@ -319,3 +319,21 @@ def test_evolve_paper_shape_seeds_vs_oracle(case, seed):
     assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
     assert [t[1] for t in r.trace] == list(o["trace_best"])
     assert [t[2] for t in r.trace] == list(o["trace_mean"])
+
+
+def test_ga_session_results_sync_and_partial_run_errors():
+    """hs_ga_result drains the session's own (non-blocking) stream before it
+    reads island states, and refuses a session that is not run to the end."""
+    import torch
+
+    from paper_2206_01288_b200 import _native as N
+    g, w = I.instance("case5")
+    cfg = S.ScheduleConfig(pop_size=32, generations=40, local_search="ours", seed=9)
+    one = S.evolve(g, w, cfg)
+    side = torch.cuda.Stream()
+    sess = S.GASession(g, w, cfg, [np.random.Generator(np.random.PCG64(9))])
+    sess.run(20, stream=side.cuda_stream)
+    with pytest.raises(N.NativeError, match="not finished"):
+        sess.results()
+    sess.run(40, stream=side.cuda_stream)  # no host synchronisation before results()
+    assert sess.results()[0].to_dict() == one.to_dict()
