@@ -41,7 +41,15 @@ const char *hs_last_error(void);
  * float64, symmetric, bw diagonal +inf) and builds the DP/PP/SW pair tables
  * (K0) and the PP rank table.  Replaces the per-call np.ix_ gathers of
  * costmodel.py:154-183 and SurrogateWeights.from_instance
- * (scheduler.py:84-88), which the reference rebuilds on every call. */
+ * (scheduler.py:84-88), which the reference rebuilds on every call.
+ * On error nothing is leaked and *h is untouched.
+ *
+ * Threading: every entry point is re-entrant per handle.  Calls on
+ * different streams never share device scratch (d_pp 9..16 / > 16 calls
+ * take a per-call scratch set from the handle's pool); the host-buffer
+ * entry serialises on the handle.  The search / GA / assignment entries
+ * raise the device's per-thread stack limit to 8 KiB if it is lower
+ * (cudaLimitStackSize, process-wide). */
 int hs_instance_create(const double *lat, const double *bw, int n, int d_pp, int d_dp, double dp_num,
                        double pp_num, double sw_num, int device, hs_instance **out);
 int hs_instance_destroy(hs_instance *h);

@@ -31,6 +31,13 @@ int fail(int code, const char* what, cudaError_t e) {
     return code;
 }
 
+int ensure_search_stack() {
+    size_t stack = 0;
+    CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "cudaDeviceGetLimit");
+    if (stack < 8192) CK(cudaDeviceSetLimit(cudaLimitStackSize, 8192), "cudaDeviceSetLimit");
+    return 0;
+}
+
 
 // Held-Karp schedule for k <= 8 (see hs_eval.cuh, warp_held_karp): compact
 // offsets off[s] (entries for |s| >= 2, s ascending), and per state (s, u)
@@ -223,26 +230,89 @@ static hs::EvalArgs base_args(const hs_instance* h) {
     return a;
 }
 
-// d_pp 9..16 without stage order: chunks of stage kernel -> cluster Held-Karp.
-// The stage kernel of chunk c+1 runs on a side stream while the Held-Karp
-// kernel of chunk c runs on `s` (the stage CTAs fit beside the cluster CTAs'
-// shared memory); ping-pong stage buffers, event-ordered.
-static int launch_two(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
-    const bool m8 = a.key16 && a.m == 8;
-    if (!h->two_E[set][0]) {
-        for (int i = 0; i < 2; i++) {
-            CK(cudaMalloc(&h->two_E[set][i], (size_t)h->two_chunk * hs::kStageStride * 8), "cudaMalloc stage graphs");
-            CK(cudaMalloc(&h->two_dp[set][i], (size_t)h->two_chunk * 8), "cudaMalloc stage datap");
-            CK(cudaMalloc(&h->two_bad[set][i], (size_t)h->two_chunk), "cudaMalloc stage flags");
-            CK(cudaEventCreateWithFlags(&h->two_ev_stage[set][i], cudaEventDisableTiming), "event");
-            CK(cudaEventCreateWithFlags(&h->two_ev_hk[set][i], cudaEventDisableTiming), "event");
-        }
-        CK(cudaStreamCreateWithFlags(&h->two_side[set], cudaStreamNonBlocking), "stream");
-        CK(cudaEventCreateWithFlags(&h->two_ev_in[set], cudaEventDisableTiming), "event");
+// ---- per-call scratch (hs_scratch, hs_instance.h) ---------------------------
+
+static void scratch_free(hs_scratch* x) {
+    for (int i = 0; i < 2; i++) {
+        if (x->two_E[i]) cudaFree(x->two_E[i]);
+        if (x->two_dp[i]) cudaFree(x->two_dp[i]);
+        if (x->two_bad[i]) cudaFree(x->two_bad[i]);
+        if (x->ev_stage[i]) cudaEventDestroy(x->ev_stage[i]);
+        if (x->ev_hk[i]) cudaEventDestroy(x->ev_hk[i]);
     }
-    cudaStream_t side = h->two_side[set];
-    CK(cudaEventRecord(h->two_ev_in[set], s), "event");  // inputs produced on s before this call
-    CK(cudaStreamWaitEvent(side, h->two_ev_in[set], 0), "wait");
+    if (x->side) cudaStreamDestroy(x->side);
+    if (x->ev_in) cudaEventDestroy(x->ev_in);
+    if (x->big) cudaFree(x->big);
+    if (x->heur_E) cudaFree(x->heur_E);
+    if (x->done) cudaEventDestroy(x->done);
+    delete x;
+}
+
+// Take a set for one call on stream s: a free one (s waits until its last
+// user's work is done) or a new one.
+static int scratch_acquire(hs_instance* h, cudaStream_t s, hs_scratch** out) {
+    hs_scratch* x = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(h->pool_mu);
+        if (!h->pool_free.empty()) {
+            x = h->pool_free.back();
+            h->pool_free.pop_back();
+        }
+    }
+    if (!x) {
+        x = new hs_scratch();
+        cudaError_t e = cudaEventCreateWithFlags(&x->done, cudaEventDisableTiming);
+        if (e != cudaSuccess) {
+            delete x;
+            return hsx::fail(-1, "event", e);
+        }
+        std::lock_guard<std::mutex> lk(h->pool_mu);
+        h->pool_all.push_back(x);
+    }
+    if (x->used) {
+        cudaError_t e = cudaStreamWaitEvent(s, x->done, 0);
+        if (e != cudaSuccess) {
+            std::lock_guard<std::mutex> lk(h->pool_mu);
+            h->pool_free.push_back(x);
+            return hsx::fail(-1, "wait", e);
+        }
+    }
+    *out = x;
+    return 0;
+}
+
+// Hand the set back once every use of it is enqueued on s (work on the
+// side stream is joined into s before this).
+static int scratch_release(hs_instance* h, hs_scratch* x, cudaStream_t s, int rc) {
+    cudaError_t e = cudaEventRecord(x->done, s);
+    x->used = true;
+    {
+        std::lock_guard<std::mutex> lk(h->pool_mu);
+        h->pool_free.push_back(x);
+    }
+    if (!rc && e != cudaSuccess) return hsx::fail(-1, "event", e);
+    return rc;
+}
+
+// d_pp 9..16 without stage order: chunks of stage kernel -> cluster Held-Karp.
+// The stage kernel of chunk c+1 runs on the set's side stream while the
+// Held-Karp kernel of chunk c runs on `s` (the stage CTAs fit beside the
+// cluster CTAs' shared memory); ping-pong stage buffers, event-ordered.
+static int launch_two(hs_instance* h, const hs::EvalArgs& a, hs_scratch* x, cudaStream_t s) {
+    const bool m8 = a.key16 && a.m == 8;
+    if (!x->two_E[0]) {
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMalloc(&x->two_E[i], (size_t)h->two_chunk * hs::kStageStride * 8), "cudaMalloc stage graphs");
+            CK(cudaMalloc(&x->two_dp[i], (size_t)h->two_chunk * 8), "cudaMalloc stage datap");
+            CK(cudaMalloc(&x->two_bad[i], (size_t)h->two_chunk), "cudaMalloc stage flags");
+            CK(cudaEventCreateWithFlags(&x->ev_stage[i], cudaEventDisableTiming), "event");
+            CK(cudaEventCreateWithFlags(&x->ev_hk[i], cudaEventDisableTiming), "event");
+        }
+        CK(cudaStreamCreateWithFlags(&x->side, cudaStreamNonBlocking), "stream");
+        CK(cudaEventCreateWithFlags(&x->ev_in, cudaEventDisableTiming), "event");
+    }
+    CK(cudaEventRecord(x->ev_in, s), "event");  // inputs produced on s before this call
+    CK(cudaStreamWaitEvent(x->side, x->ev_in, 0), "wait");
     int64_t c = 0;
     for (int64_t lo = 0; lo < a.P; lo += h->two_chunk, c++) {
         const int i = (int)(c & 1);
@@ -252,57 +322,57 @@ static int launch_two(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream
         ca.P = cnt;
         ca.datap = a.datap ? a.datap + lo : nullptr;
         ca.per_group = a.per_group ? a.per_group + lo * a.k : nullptr;
-        if (c >= 2) CK(cudaStreamWaitEvent(side, h->two_ev_hk[set][i], 0), "wait");  // buffer i is free again
-        if (hs::launch_stage(ca, h->two_E[set][i], h->two_dp[set][i], h->two_bad[set][i], h->stage_blocks, m8, side))
+        if (c >= 2) CK(cudaStreamWaitEvent(x->side, x->ev_hk[i], 0), "wait");  // buffer i is free again
+        if (hs::launch_stage(ca, x->two_E[i], x->two_dp[i], x->two_bad[i], h->stage_blocks, m8, x->side))
             return hsx::fail(-1, "stage launch", cudaGetLastError());
-        CK(cudaEventRecord(h->two_ev_stage[set][i], side), "event");
-        CK(cudaStreamWaitEvent(s, h->two_ev_stage[set][i], 0), "wait");
-        if (hs::launch_hk_cluster(h->two_E[set][i], hs::kStageES, hs::kStageStride, a.k, cnt, h->two, h->two_grid,
-                                  h->two_dp[set][i], h->two_bad[set][i], a.total + lo, a.pipe ? a.pipe + lo : nullptr,
-                                  s))
+        CK(cudaEventRecord(x->ev_stage[i], x->side), "event");
+        CK(cudaStreamWaitEvent(s, x->ev_stage[i], 0), "wait");
+        if (hs::launch_hk_cluster(x->two_E[i], hs::kStageES, hs::kStageStride, a.k, cnt, h->two, h->two_grid,
+                                  x->two_dp[i], x->two_bad[i], a.total + lo, a.pipe ? a.pipe + lo : nullptr, s))
             return hsx::fail(-1, "cluster Held-Karp launch", cudaGetLastError());
-        CK(cudaEventRecord(h->two_ev_hk[set][i], s), "event");
+        CK(cudaEventRecord(x->ev_hk[i], s), "event");
     }
     return 0;
 }
 
-static int launch_any(hs_instance* h, const hs::EvalArgs& a, int set, cudaStream_t s) {
-    if (h->k > 16) return hsx::fail(-3, "exact pricing is limited to d_pp <= 16 (Held-Karp); use heuristic paths");
-    if (h->k > hs::kWarpK && !a.order && h->two.rwords) return launch_two(h, a, set, s);
-    if (h->k > hs::kWarpK)
-        return hs::launch_eval_cta(a, h->hkb, h->big_scratch[set], h->big_blocks,
-                                   a.key16 && a.m == 8, s);
-    if (hs::eval8_applicable(a, h->smem_optin)) return hs::launch_eval8(a, h->sm_count, s);
-    return hs::launch_eval(a, h->plan, s);
+static int launch_cta(hs_instance* h, const hs::EvalArgs& a, hs_scratch* x, cudaStream_t s) {
+    if (!x->big) CK(cudaMalloc(&x->big, (size_t)h->big_blocks * hs::hk_big_size(h->k) * 8), "cudaMalloc scratch");
+    return hs::launch_eval_cta(a, h->hkb, x->big, h->big_blocks, a.key16 && a.m == 8, s);
 }
 
-extern "C" {
+static int launch_heur(hs_instance* h, const hs::EvalArgs& a, hs_scratch* x, cudaStream_t s) {
+    if (!x->heur_E) CK(cudaMalloc(&x->heur_E, (size_t)h->big_blocks * h->k * h->k * 8), "cudaMalloc heuristic E");
+    if (hs::launch_eval_heur(a, x->heur_E, h->big_blocks, s)) return hsx::fail(-1, "heuristic eval launch");
+    return 0;
+}
 
-int hs_version(void) { return 1; }
+static int launch_any(hs_instance* h, const hs::EvalArgs& a, cudaStream_t s) {
+    if (h->k > 16) return hsx::fail(-3, "exact pricing is limited to d_pp <= 16 (Held-Karp); use heuristic paths");
+    if (h->k <= hs::kWarpK) {  // no per-call scratch
+        const int rc = hs::eval8_applicable(a, h->smem_optin) ? hs::launch_eval8(a, h->sm_count, s)
+                                                               : hs::launch_eval(a, h->plan, s);
+        return rc ? hsx::fail(-1, "eval launch", cudaGetLastError()) : 0;
+    }
+    hs_scratch* x = nullptr;
+    int rc = scratch_acquire(h, s, &x);
+    if (rc) return rc;
+    if (!a.order && h->two.rwords) {
+        rc = launch_two(h, a, x, s);
+    } else {
+        rc = launch_cta(h, a, x, s);
+        if (rc > 0 || (rc < 0 && hsx::g_err.empty())) rc = hsx::fail(-1, "eval launch", cudaGetLastError());
+    }
+    return scratch_release(h, x, s, rc);
+}
 
-const char* hs_last_error(void) { return g_err.c_str(); }
-
-int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int d_dp, double dp_num,
-                       double pp_num, double sw_num, int device, hs_instance** out) {
-    if (!out || !lat || !bw) return fail(-2, "null argument");
-    if (n < 1 || d_pp < 1 || d_dp < 1 || (int64_t)d_pp * d_dp != n) return fail(-2, "d_pp*d_dp must equal n");
-    if (d_dp > hs::kMaxM) return fail(-3, "d_dp > 64 is not supported");
-    if (d_pp > 64) return fail(-3, "d_pp > 64 is not supported");
-    if (n > 32767) return fail(-3, "n > 32767 is not supported (int16 device ids)");
-    DeviceGuard dg(device);
-    hs_instance* h = new hs_instance();
-    h->device = device;
-    h->n = n;
-    h->k = d_pp;
-    h->m = d_dp;
+// Tables and schedules of a new handle; any error leaves partial state for
+// hs_instance_destroy to free.
+static int instance_init(hs_instance* h, const double* lat, const double* bw, double dp_num, double pp_num,
+                         double sw_num) {
+    const int n = h->n, d_pp = h->k, d_dp = h->m;
     cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    CK(cudaGetDeviceProperties(&prop, h->device), "cudaGetDeviceProperties");
     h->sm_count = prop.multiProcessorCount;
-    // the search kernels' call chains (GA driver -> crossover / passes ->
-    // warp evaluator) need more than the default 1 KiB per-thread stack
-    size_t stack = 0;
-    CK(cudaDeviceGetLimit(&stack, cudaLimitStackSize), "cudaDeviceGetLimit");
-    if (stack < 8192) CK(cudaDeviceSetLimit(cudaLimitStackSize, 8192), "cudaDeviceSetLimit");
     h->smem_optin = prop.sharedMemPerBlockOptin;
     size_t nn = (size_t)n * n;
     CK(cudaMalloc(&h->lat, nn * 8), "cudaMalloc");
@@ -327,28 +397,55 @@ int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int
         if (hs::launch_narrow((int64_t)nn, h->rank, h->rank16, 0)) return fail(-1, "narrow launch");
     }
     CK(cudaDeviceSynchronize(), "instance tables");
-    int rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk, false);
-    if (!rc) rc = get_hk(device, std::min(d_pp, (int)hs::kWarpK), &h->hk_roll, true);
+    int rc = get_hk(h->device, std::min(d_pp, (int)hs::kWarpK), &h->hk, false);
+    if (!rc) rc = get_hk(h->device, std::min(d_pp, (int)hs::kWarpK), &h->hk_roll, true);
     if (rc) return rc;
     if (d_pp > 16) {
         // exact pricing is limited to 16 stages (combinatorics.py:243-249);
         // such instances serve the heuristic and pass-only entry points
         h->big_blocks = 2 * h->sm_count;
-        CK(cudaMalloc(&h->heur_E, (size_t)h->big_blocks * d_pp * d_pp * 8), "cudaMalloc heuristic E");
     } else if (d_pp > hs::kWarpK) {
-        rc = get_hk_big(device, d_pp, &h->hkb);
+        rc = get_hk_big(h->device, d_pp, &h->hkb);
         if (rc) return rc;
         h->big_blocks = hs::big_blocks(h->sm_count, d_pp);
-        if (!hs::get_hk_two(device, d_pp, &h->two)) {
+        if (!hs::get_hk_two(h->device, d_pp, &h->two)) {
             h->two_grid = hs::cluster_grid(h->two, h->sm_count);
             h->stage_blocks = h->sm_count * 16;
             h->two_chunk = 1024;
         }
-        for (int i = 0; i < 2; i++)
-            CK(cudaMalloc(&h->big_scratch[i], (size_t)h->big_blocks * hs::hk_big_size(d_pp) * 8), "cudaMalloc scratch");
     } else {
         hs::EvalArgs a = base_args(h);
         if (hs::eval_plan(a, h->sm_count, h->smem_optin, &h->plan)) return fail(-3, "shape does not fit shared memory");
+    }
+    return 0;
+}
+
+
+extern "C" {
+
+int hs_version(void) { return 1; }
+
+const char* hs_last_error(void) { return g_err.c_str(); }
+
+int hs_instance_create(const double* lat, const double* bw, int n, int d_pp, int d_dp, double dp_num,
+                       double pp_num, double sw_num, int device, hs_instance** out) {
+    if (!out || !lat || !bw) return fail(-2, "null argument");
+    if (n < 1 || d_pp < 1 || d_dp < 1 || (int64_t)d_pp * d_dp != n) return fail(-2, "d_pp*d_dp must equal n");
+    if (d_dp > hs::kMaxM) return fail(-3, "d_dp > 64 is not supported");
+    if (d_pp > 64) return fail(-3, "d_pp > 64 is not supported");
+    if (n > 32767) return fail(-3, "n > 32767 is not supported (int16 device ids)");
+    DeviceGuard dg(device);
+    hs_instance* h = new hs_instance();
+    h->device = device;
+    h->n = n;
+    h->k = d_pp;
+    h->m = d_dp;
+    const int rc = instance_init(h, lat, bw, dp_num, pp_num, sw_num);
+    if (rc) {  // free whatever the partial init allocated
+        const std::string err = g_err;
+        hs_instance_destroy(h);
+        g_err = err;
+        return rc;
     }
     *out = h;
     return 0;
@@ -365,20 +462,7 @@ int hs_instance_destroy(hs_instance* h) {
     cudaFree(h->vals);
     cudaFree(h->rank);
     if (h->rank16) cudaFree(h->rank16);
-    for (int i = 0; i < 2; i++)
-        if (h->big_scratch[i]) cudaFree(h->big_scratch[i]);
-    for (int i = 0; i < 2; i++) {
-        for (int j = 0; j < 2; j++) {
-            if (h->two_E[i][j]) cudaFree(h->two_E[i][j]);
-            if (h->two_dp[i][j]) cudaFree(h->two_dp[i][j]);
-            if (h->two_bad[i][j]) cudaFree(h->two_bad[i][j]);
-            if (h->two_ev_stage[i][j]) cudaEventDestroy(h->two_ev_stage[i][j]);
-            if (h->two_ev_hk[i][j]) cudaEventDestroy(h->two_ev_hk[i][j]);
-        }
-        if (h->two_side[i]) cudaStreamDestroy(h->two_side[i]);
-        if (h->two_ev_in[i]) cudaEventDestroy(h->two_ev_in[i]);
-    }
-    if (h->heur_E) cudaFree(h->heur_E);
+    for (hs_scratch* x : h->pool_all) scratch_free(x);
     cudaFree(h->invalid);
     for (int i = 0; i < 2; i++) {
         if (h->cg[i]) cudaFree(h->cg[i]);
@@ -416,7 +500,8 @@ int hs_eval_batch(hs_instance* h, const int16_t* groups, int64_t P, double* tota
     a.per_group = per_group;
     a.order = order;
     a.invalid = invalid ? invalid : h->invalid;
-    if (launch_any(h, a, 0, (cudaStream_t)stream)) return fail(-1, "eval launch", cudaGetLastError());
+    int rc = launch_any(h, a, (cudaStream_t)stream);
+    if (rc) return rc;
     return 0;
 }
 
@@ -437,9 +522,11 @@ int hs_eval_batch_ex(hs_instance* h, const int16_t* groups, int64_t P, double* t
     a.per_group = per_group;
     a.order = order;
     a.invalid = invalid ? invalid : h->invalid;
-    if (hs::launch_eval_heur(a, h->heur_E, h->big_blocks, (cudaStream_t)stream))
-        return fail(-1, "heuristic eval launch", cudaGetLastError());
-    return 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    hs_scratch* x = nullptr;
+    int rc = scratch_acquire(h, s, &x);
+    if (rc) return rc;
+    return scratch_release(h, x, s, launch_heur(h, a, x, s));
 }
 
 int hs_path_heuristic_batch(const double* w, int k, int64_t B, double* total, int8_t* order, int device, void* stream) {
@@ -497,7 +584,8 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
         a.pipe = h->co[b] + 2 * h->chunk;
         a.per_group = per_group ? h->co[b] + 3 * h->chunk : nullptr;
         a.order = order ? reinterpret_cast<int8_t*>(h->co[b] + (3 + h->k) * h->chunk) : nullptr;
-        if (launch_any(h, a, b, s)) return fail(-1, "eval launch", cudaGetLastError());
+        int rc = launch_any(h, a, s);
+        if (rc) return rc;
         CK(cudaMemcpyAsync(total + lo, a.total, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
         if (datap) CK(cudaMemcpyAsync(datap + lo, a.datap, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
         if (pipelinep) CK(cudaMemcpyAsync(pipelinep + lo, a.pipe, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");

@@ -25,6 +25,7 @@ int hs_materialize(hs_instance* h, int64_t B, const int16_t* groups, int16_t* gr
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (h->k > 8) return fail(-3, "GPU materialize covers d_pp <= 8");
     DeviceGuard dg(h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     const int km = h->k * h->m;
     Buf<int16_t> g, gr;
     Buf<int8_t> od;
@@ -58,6 +59,7 @@ int hs_evaluate_assignments(hs_instance* h, int64_t B, const int16_t* grids, dou
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (h->k > 16) return fail(-3, "d_pp > 16");
     DeviceGuard dg(h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     const int km = h->k * h->m;
     Buf<int16_t> g;
     Buf<double> o, pc;
@@ -77,6 +79,7 @@ int hs_random_assignments(int n, int d_pp, int d_dp, int device, int B, hs_pcg64
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (n != d_pp * d_dp || n > 32767 || d_pp > 64) return fail(-2, "bad shape");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     Buf<hs_pcg64> r;
     Buf<int16_t> sc, gr;
     Buf<int8_t> od;
@@ -99,6 +102,7 @@ int hs_bottleneck_match_batch(const double* w, int m, int64_t B, double* value, 
     if (B < 0) return fail(-2, "negative batch");
     if (B && (!w || !value)) return fail(-2, "null argument");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     if (hs::launch_bottleneck_match(w, m, B, value, pairs, (cudaStream_t)stream))
         return fail(-1, "bottleneck matching launch", cudaGetLastError());
     return 0;
@@ -110,6 +114,7 @@ int hs_datap_group_batch(const double* lat, const double* bw, int m, int64_t G, 
     if (G < 0) return fail(-2, "negative batch");
     if (G && (!lat || !bw || !out)) return fail(-2, "null argument");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     if (hs::launch_datap_group(lat, bw, m, G, ddp, dp_num, out, (cudaStream_t)stream))
         return fail(-1, "datap group launch", cudaGetLastError());
     return 0;

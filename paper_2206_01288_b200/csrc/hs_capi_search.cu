@@ -120,6 +120,7 @@ int hs_ga_create_ex(hs_instance* h, const hs_ga_config* cfg, int islands, const 
     int rc = check_search_shape(h, cfg->kind, cfg->max_passes);
     if (rc) return rc;
     DeviceGuard dg(h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     hs_ga* ga = new hs_ga();
     ga->h = h;
     ga->cfg = *cfg;
@@ -157,6 +158,7 @@ int hs_ga_create_ex(hs_instance* h, const hs_ga_config* cfg, int islands, const 
 int hs_ga_run(hs_ga* ga, int until, void* stream) {
     if (!ga) return fail(-2, "null handle");
     DeviceGuard dg(ga->h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     until = std::min(until, ga->cfg.generations);
     hs::GAArgs a = ga_args(ga, until, until >= ga->cfg.generations);
     if (hs::launch_ga(a, ga->plan, ga->islands, ga->h->rank16 != nullptr, (cudaStream_t)stream))
@@ -169,6 +171,7 @@ int hs_ga_export(hs_ga* ga, int elites, int16_t* groups, double* costs, void* st
     if (!ga) return fail(-2, "null handle");
     if (elites < 1 || elites > ga->cfg.pop_size) return fail(-2, "elites must be in 1..pop_size");
     DeviceGuard dg(ga->h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     if (hs::launch_export(ga->islands, ga->cfg.pop_size, ga->h->k * ga->h->m, elites, ga->pop, ga->cost, groups, costs,
                           (cudaStream_t)stream))
         return fail(-1, "export launch", cudaGetLastError());
@@ -180,6 +183,7 @@ int hs_ga_import(hs_ga* ga, int elites, const int16_t* groups, const double* cos
     if (!ga) return fail(-2, "null handle");
     if (elites < 1 || elites > ga->cfg.pop_size) return fail(-2, "elites must be in 1..pop_size");
     DeviceGuard dg(ga->h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     if (hs::launch_import(ga->islands, ga->cfg.pop_size, ga->h->k * ga->h->m, elites, ga->pop, ga->cost, ga->best,
                           ga->state, groups, costs, src, (cudaStream_t)stream))
         return fail(-1, "import launch", cudaGetLastError());
@@ -191,6 +195,7 @@ int hs_ga_result(hs_ga* ga, int16_t* best_groups, double* best3, double* best_pe
                  double* trace_best, double* trace_mean, int32_t* trace_len, int64_t* evaluations, hs_pcg64* rng) {
     if (!ga) return fail(-2, "null handle");
     DeviceGuard dg(ga->h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     // the session's work may still be in flight on the caller's (possibly
     // non-blocking) stream: drain it before reading the island states
     CK(cudaStreamSynchronize(ga->last), "ga sync");
@@ -256,6 +261,7 @@ static int refine_common(hs_instance* h, int kind, int max_passes, int single, i
     int rc = check_search_shape(h, kind, max_passes);
     if (rc) return rc;
     DeviceGuard dg(h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     hs::SearchPlan plan;
     if (hs::search_plan(shape_of(h, max_passes), 2, h->smem_optin, &plan)) return fail(-3, "does not fit smem");
     const int km = h->k * h->m;
@@ -320,6 +326,7 @@ int hs_refine_pass(hs_instance* h, int kind, int phase, int B, const int16_t* gr
         return fail(-4, "zero-size array to reduction operation maximum which has no identity");
     if (h->k > 32 || h->m > 64) return fail(-3, "passes support d_pp <= 32, d_dp <= 64");
     DeviceGuard dg(h->device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     const int km = h->k * h->m;
     DevBuf<int16_t> gi, go;
     DevBuf<hs_pcg64> r;
@@ -360,6 +367,7 @@ int hs_crossover(int n, int d_pp, int d_dp, int device, int B, const int16_t* p1
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (n != d_pp * d_dp || d_dp > 64 || n > 32767) return fail(-2, "bad shape");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     const int km = n;
     DevBuf<int16_t> a1, a2, o;
     DevBuf<hs_pcg64> r;
@@ -382,6 +390,7 @@ int hs_gains(int n, int d_pp, int d_dp, int device, const double* sw, int kind, 
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (n != d_pp * d_dp || d_dp > 64) return fail(-2, "bad shape");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     DevBuf<int16_t> g;
     DevBuf<int32_t> dq;
     DevBuf<double> o, w;
@@ -401,6 +410,7 @@ int hs_random_partitions(int n, int d_pp, int d_dp, int device, int B, hs_pcg64*
     if (B <= 0) return B == 0 ? 0 : fail(-2, "negative batch");
     if (n != d_pp * d_dp || n > 32767) return fail(-2, "bad shape");
     DeviceGuard dg(device);
+    if (int rc_ = hsx::ensure_search_stack()) return rc_;
     DevBuf<int16_t> o;
     DevBuf<hs_pcg64> r;
     CK(o.alloc((size_t)B * n), "cudaMalloc");

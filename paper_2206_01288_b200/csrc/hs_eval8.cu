@@ -17,20 +17,37 @@
 // Tables staged once per persistent CTA: the Held-Karp offset rows, the u16
 // rank table and the DP table (odd row strides).  Outputs are bit-identical
 // to the schedule-driven warp kernel (hs_kernels.cu) and to the reference.
+//
+// Occupancy: a Held-Karp block set (4 candidate blocks, 19.2 KB) is needed
+// only during the Held-Karp phase (about a third of a quad's instructions),
+// so the CTA's 16 warps share kE8Sets < 16 sets from a free mask in shared
+// memory: a warp computes its matchings with the edge values in registers,
+// takes a free set, writes the edges, runs Held-Karp and hands the set back.
+// That doubles the resident warps (16 per SM at <= 128 registers) that the
+// 227 KB of shared memory allowed with one private set per warp.
 #include "hs_hk8_gen.cuh"
 #include "hs_match8_dp.cuh"
 #include "hs_warp_eval.cuh"
 
 namespace hs {
 
-constexpr int kE8Warps = 8;
+#ifndef HS_E8_WARPS
+#define HS_E8_WARPS 16
+#endif
+constexpr int kE8Warps = HS_E8_WARPS;
 constexpr int kE8DS = 65;  // DP row stride (doubles)
 constexpr int kE8RS = 66;  // rank row stride (u16): 33 words, odd
 constexpr size_t kE8OffBytes = (size_t)8 * kHK8Words * 4 + 64;  // + layer-2 edge slots
 constexpr size_t kE8RkBytes = ((size_t)64 * kE8RS * 2 + 15) & ~(size_t)15;
 constexpr size_t kE8DpBytes = (size_t)64 * kE8DS * 8;
-constexpr size_t kE8WarpBytes = (size_t)4 * kHK8Block * 8 + 4 * 64 * 2;
-constexpr size_t kE8Smem = kE8OffBytes + kE8RkBytes + kE8DpBytes + kE8Warps * kE8WarpBytes;
+constexpr size_t kE8MemBytes = (size_t)4 * 64 * 2;             // per warp: the quad's groups
+constexpr size_t kE8SetBytes = (size_t)4 * kHK8Block * 8;      // one Held-Karp block set
+constexpr size_t kE8Fixed = kE8OffBytes + kE8RkBytes + kE8DpBytes + kE8Warps * kE8MemBytes + 16;
+constexpr size_t kE8SmemCap = 232448;                          // sm_100 opt-in maximum per CTA
+constexpr int kE8Sets = (int)((kE8SmemCap - kE8Fixed) / kE8SetBytes) < kE8Warps
+                            ? (int)((kE8SmemCap - kE8Fixed) / kE8SetBytes) : kE8Warps;
+constexpr size_t kE8Smem = kE8Fixed + (size_t)kE8Sets * kE8SetBytes;
+static_assert(kE8Sets >= 1, "no Held-Karp block set fits");
 
 __device__ __forceinline__ double shfl_xor_d(double x, int m) {
     return __longlong_as_double(__shfl_xor_sync(0xffffffffu, __double_as_longlong(x), m));
@@ -44,11 +61,14 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
     uint32_t* offs = reinterpret_cast<uint32_t*>(smem);
     uint16_t* rk = reinterpret_cast<uint16_t*>(smem + kE8OffBytes);
     double* dp = reinterpret_cast<double*>(smem + kE8OffBytes + kE8RkBytes);
-    unsigned char* wsm = smem + kE8OffBytes + kE8RkBytes + kE8DpBytes;
+    unsigned char* memsm = smem + kE8OffBytes + kE8RkBytes + kE8DpBytes;
+    unsigned* freemask = reinterpret_cast<unsigned*>(memsm + kE8Warps * kE8MemBytes);
+    char* sets = reinterpret_cast<char*>(memsm + kE8Warps * kE8MemBytes + 16);
     const uint16_t* grk = reinterpret_cast<const uint16_t*>(a.rank);
     uint16_t* eslot = reinterpret_cast<uint16_t*>(offs + 8 * kHK8Words);
     for (int i = threadIdx.x; i < 8 * kHK8Words; i += blockDim.x) offs[i] = kHK8Offs[i];
     if (threadIdx.x < 28) eslot[threadIdx.x] = kHK8Edge[threadIdx.x];
+    if (threadIdx.x == 0) *freemask = kE8Sets == 32 ? 0xffffffffu : (1u << kE8Sets) - 1u;
     for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
         const int r = i >> 6, c = i & 63;
         rk[r * kE8RS + c] = grk[i];
@@ -58,9 +78,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int c = lane >> 3, g = lane & 7;
-    char* blocks = reinterpret_cast<char*>(wsm + (size_t)wid * kE8WarpBytes);
-    char* blk = blocks + (size_t)c * kHK8Block * 8;
-    int16_t* memw = reinterpret_cast<int16_t*>(blocks + (size_t)4 * kHK8Block * 8);
+    int16_t* memw = reinterpret_cast<int16_t*>(memsm + (size_t)wid * kE8MemBytes);
     const uint4* t4 = reinterpret_cast<const uint4*>(offs + g * kHK8Words);
     const double nan = __longlong_as_double(0x7ff8000000000000LL);
     const uint4* gsrc = reinterpret_cast<const uint4*>(a.groups);
@@ -112,31 +130,73 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
 #pragma unroll
         for (int m = 1; m < 8; m <<= 1) datap = dmax(datap, shfl_xor_d(datap, m));
         __syncwarp();
-        // pipeline edges: 4 x 28 group pairs over 32 lanes
+        // pipeline edges: 4 x 28 group pairs over 32 lanes (t = lane + 32 i),
+        // kept in registers until the warp holds a Held-Karp set
+        double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll 1
-        for (int t = lane; t < 112; t += 32) {
-            const int cc = t / 28, pi = t - cc * 28;
-            int j, j2;
-            decode_pair(pi, 8, j, j2);
-            const uint4 A4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j];
-            const uint4 B4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j2];
-            const uint32_t Aw[4] = {A4.x, A4.y, A4.z, A4.w};
-            const uint32_t Bw[4] = {B4.x, B4.y, B4.z, B4.w};
-            int b[8];
+        for (int i = 0; i < 4; i++) {
+            const int t = lane + 32 * i;
+            if (t < 112) {
+                const int cc = t / 28, pi = t - cc * 28;
+                int j, j2;
+                decode_pair(pi, 8, j, j2);
+                const uint4 A4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j];
+                const uint4 B4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j2];
+                const uint32_t Aw[4] = {A4.x, A4.y, A4.z, A4.w};
+                const uint32_t Bw[4] = {B4.x, B4.y, B4.z, B4.w};
+                int b[8];
 #pragma unroll
-            for (int i = 0; i < 8; i++) b[i] = i16(Bw[i >> 1], i & 1);
-            const uint32_t L = match8_dp([&](int r, uint32_t(&kn)[4]) {
-                const uint16_t* row = rk + i16(Aw[r >> 1], r & 1) * kE8RS;
+                for (int k = 0; k < 8; k++) b[k] = i16(Bw[k >> 1], k & 1);
+                const uint32_t L = match8_dp([&](int r, uint32_t(&kn)[4]) {
+                    const uint16_t* row = rk + i16(Aw[r >> 1], r & 1) * kE8RS;
 #pragma unroll
-                for (int qq = 0; qq < 4; qq++) kn[qq] = (uint32_t)row[b[qq]] | ((uint32_t)row[b[qq + 4]] << 16);
-            });
-            const double e = __ldg(a.vals + L);
-            double* dst = reinterpret_cast<double*>(blocks) + cc * kHK8Block + eslot[pi];
-            dst[0] = e;  // h[{j, j2}][j] and h[{j, j2}][j2]
-            dst[kHK8EdgeStride] = e;
+                    for (int qq = 0; qq < 4; qq++)
+                        kn[qq] = (uint32_t)row[b[qq]] | ((uint32_t)row[b[qq + 4]] << 16);
+                });
+                const double v = __ldg(a.vals + L);
+                e0 = i == 0 ? v : e0;
+                e1 = i == 1 ? v : e1;
+                e2 = i == 2 ? v : e2;
+                e3 = i == 3 ? v : e3;
+            }
+        }
+        const double e[4] = {e0, e1, e2, e3};
+        // take a free Held-Karp set
+        int set = 0;
+        if (lane == 0) {
+            unsigned old = *reinterpret_cast<volatile unsigned*>(freemask);
+            for (;;) {
+                if (old) {
+                    set = __ffs(old) - 1;
+                    const unsigned prev = atomicAnd(freemask, ~(1u << set));
+                    if (prev & (1u << set)) break;
+                    old = prev & ~(1u << set);
+                } else {
+                    __nanosleep(32);
+                    old = *reinterpret_cast<volatile unsigned*>(freemask);
+                }
+            }
+            __threadfence_block();
+        }
+        set = __shfl_sync(0xffffffffu, set, 0);
+        char* blocks = sets + (size_t)set * kE8SetBytes;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int t = lane + 32 * i;
+            if (t < 112) {
+                const int cc = t / 28, pi = t - cc * 28;
+                double* dst = reinterpret_cast<double*>(blocks) + cc * kHK8Block + eslot[pi];
+                dst[0] = e[i];  // h[{j, j2}][j] and h[{j, j2}][j2]
+                dst[kHK8EdgeStride] = e[i];
+            }
         }
         __syncwarp();
-        double pipe = hk8_lane(blk, t4);
+        double pipe = hk8_lane(blocks + (size_t)c * kHK8Block * 8, t4);
+        __syncwarp();  // every lane is done with the set
+        if (lane == 0) {
+            __threadfence_block();
+            atomicOr(freemask, 1u << set);
+        }
 #pragma unroll
         for (int m = 1; m < 8; m <<= 1) pipe = dmin(pipe, shfl_xor_d(pipe, m));
         if (live) {
@@ -168,7 +228,8 @@ bool eval8_applicable(const EvalArgs& a, size_t smem_optin) {
 int launch_eval8(const EvalArgs& a, int sm_count, cudaStream_t s) {
     if (a.P == 0) return 0;
     const int64_t quads = (a.P + 3) / 4;
-    const int blocks = (int)std::min<int64_t>(sm_count, (quads + kE8Warps - 1) / kE8Warps);
+    // small batches: spread the quads over every SM (a quad's latency is the floor)
+    const int blocks = (int)std::min<int64_t>(sm_count, quads);
     if (a.per_group) {
         cudaFuncSetAttribute(eval8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
         eval8_kernel<true><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);

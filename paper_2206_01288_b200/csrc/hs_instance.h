@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/hetsched_b200.h"
 #include "hs_cluster.h"
@@ -13,6 +14,11 @@ namespace hsx {
 int fail(int code, const char* what, cudaError_t e = cudaSuccess);
 int get_hk(int device, int k, hs::HKTables* out, bool roll = false);
 int get_hk_big(int device, int k, hs::HKBig* out);
+// The search / assignment kernels' call chains (GA driver -> crossover /
+// passes -> warp evaluator) need more than the default 1 KiB per-thread
+// stack: raise the current device's limit to 8 KiB if it is lower (a
+// process-wide setting; documented in include/hetsched_b200.h).
+int ensure_search_stack();
 
 struct DeviceGuard {
     int prev = -1;
@@ -35,6 +41,23 @@ struct DeviceGuard {
         if (e_ != cudaSuccess) return hsx::fail(-1, what, e_);      \
     } while (0)
 
+// Per-call device scratch of the d_pp > 8 eval paths.  A call takes a set
+// from the handle's pool (a new one when every set is in use), so calls on
+// different streams never share buffers; a set handed back records `done`
+// on the call's stream and its next user waits on that event before
+// touching the buffers (HS C-ABI re-entrancy).
+struct hs_scratch {
+    double* two_E[2] = {};        // stage graphs, ping-pong (stage + cluster Held-Karp)
+    double* two_dp[2] = {};
+    uint8_t* two_bad[2] = {};
+    cudaStream_t side = nullptr;  // stage kernels beside the Held-Karp kernel
+    cudaEvent_t ev_stage[2] = {}, ev_hk[2] = {}, ev_in = nullptr;
+    double* big = nullptr;        // per-CTA Held-Karp slices (eval_cta_kernel, stage order wanted)
+    double* heur_E = nullptr;     // d_pp > 16: per-CTA stage graphs of the heuristic path
+    cudaEvent_t done = nullptr;   // recorded on the last user's stream
+    bool used = false;
+};
+
 struct hs_instance {
     int device = 0, n = 0, k = 0, m = 0, sm_count = 0;
     size_t smem_optin = 0;
@@ -45,18 +68,14 @@ struct hs_instance {
     hs::HKTables hk{};
     hs::HKTables hk_roll{};        // two-layer schedule: batch pricing without stage order
     hs::HKBig hkb{};               // d_pp > 8: CTA evaluator schedule
-    double* big_scratch[2] = {nullptr, nullptr};  // per-CTA Held-Karp slices (two stream sets)
     int big_blocks = 0;
     // d_pp 9..16 without stage order: stage kernel + cluster Held-Karp (hs_cluster.cu)
     hs::HKTwo two{};
     int two_grid = 0, stage_blocks = 0;
     int64_t two_chunk = 0;
-    double* two_E[2][2] = {};     // [stream set][ping-pong]
-    double* two_dp[2][2] = {};
-    uint8_t* two_bad[2][2] = {};
-    cudaStream_t two_side[2] = {};
-    cudaEvent_t two_ev_stage[2][2] = {}, two_ev_hk[2][2] = {}, two_ev_in[2] = {};
-    double* heur_E = nullptr;      // d_pp > 16: per-CTA stage graphs for the heuristic path
+    // scratch pool (hs_scratch above)
+    std::mutex pool_mu;
+    std::vector<hs_scratch*> pool_all, pool_free;
     int* invalid = nullptr;
     hs::EvalPlan plan{};
     // host-buffer path

@@ -315,3 +315,46 @@ def test_multi_device_split_device_tensor_and_errors():
     bad[-1, 0, 0] = bad[-1, 0, 1]
     with pytest.raises(hs.CostModelError, match="1 of 5003"):
         hs.comm_cost_batch(g, bad, w, devices=_devices_for_split())
+
+
+def test_two_streams_concurrently_on_one_config4_handle():
+    """Per-handle re-entrancy: d_pp = 16 calls on two
+    streams of one handle run concurrently with private scratch sets, the
+    stage-kernel + cluster path (no order) on one and the CTA path (with
+    order) on the other, twice each; all must equal the oracle."""
+    import torch
+
+    from paper_2206_01288_b200 import _native as N
+    from paper_2206_01288_b200.costmodel import _launch_device
+    g, w = I.instance("config4")
+    inst = N.instance_for(g, w)
+    a = _random_parts(31, 24, 512, 16, 32)
+    b = _random_parts(32, 24, 512, 16, 32)
+    orc = O.Oracle.of(g, w)
+    want_a = orc.comm_cost_batch(a, threads=O.cpu_count())[0]
+    want_b = orc.comm_cost_batch(b, threads=O.cpu_count())[0]
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(2):
+        with torch.cuda.stream(s1):
+            outs.append(("a", _launch_device(inst, ta, False, False)))
+        with torch.cuda.stream(s2):
+            outs.append(("b", _launch_device(inst, tb, True, True)))
+    torch.cuda.synchronize()
+    for which, (out, bad) in outs:
+        assert int(bad.item()) == 0
+        want = want_a if which == "a" else want_b
+        assert np.array_equal(out["total"].cpu().numpy(), want), which
+
+
+def test_host_path_from_two_threads_on_one_handle():
+    from concurrent.futures import ThreadPoolExecutor
+    g, w = I.instance("case1")
+    pops = [_random_parts(40 + i, 70_000, 64, 8, 8) for i in range(4)]
+    ref = [hs.comm_cost_batch(g, p, w)["total"] for p in pops]
+    with ThreadPoolExecutor(4) as ex:
+        got = list(ex.map(lambda p: hs.comm_cost_batch(g, p, w)["total"], pops))
+    for r, x in zip(ref, got):
+        assert np.array_equal(r, x)
