@@ -87,6 +87,22 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
                                    (uint32_t)(8 * g + 4) | (uint32_t)(8 * g + 5) << 16,
                                    (uint32_t)(8 * g + 6) | (uint32_t)(8 * g + 7) << 16);
 
+    // this lane's share of the quad's 112 group pairs, t = lane + 32 i (loop
+    // invariant): A-group row | B-group row << 8 | edge slot << 16 (0 = none)
+    uint32_t job[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const int t = lane + 32 * i;
+        job[i] = 0;
+        if (t < 112) {
+            const int cc = t / 28, pi = t - cc * 28;
+            int j, j2;
+            decode_pair(pi, 8, j, j2);
+            job[i] = (uint32_t)(cc * 8 + j) | (uint32_t)(cc * 8 + j2) << 8 |
+                     (uint32_t)(cc * kHK8Block + eslot[pi]) << 16;
+        }
+    }
+
     for (int64_t q = (int64_t)blockIdx.x * W + wid; q * 4 < a.P; q += (int64_t)gridDim.x * W) {
         const int64_t p = q * 4 + c;
         const bool live = p < a.P;
@@ -135,13 +151,10 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll 1
         for (int i = 0; i < 4; i++) {
-            const int t = lane + 32 * i;
-            if (t < 112) {
-                const int cc = t / 28, pi = t - cc * 28;
-                int j, j2;
-                decode_pair(pi, 8, j, j2);
-                const uint4 A4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j];
-                const uint4 B4 = reinterpret_cast<const uint4*>(memw)[cc * 8 + j2];
+            const uint32_t jb = i == 0 ? job[0] : i == 1 ? job[1] : i == 2 ? job[2] : job[3];
+            if (jb) {
+                const uint4 A4 = reinterpret_cast<const uint4*>(memw)[jb & 0xFFu];
+                const uint4 B4 = reinterpret_cast<const uint4*>(memw)[(jb >> 8) & 0xFFu];
                 const uint32_t Aw[4] = {A4.x, A4.y, A4.z, A4.w};
                 const uint32_t Bw[4] = {B4.x, B4.y, B4.z, B4.w};
                 int b[8];
@@ -150,8 +163,12 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
                 const uint32_t L = match8_dp([&](int r, uint32_t(&kn)[4]) {
                     const uint16_t* row = rk + i16(Aw[r >> 1], r & 1) * kE8RS;
 #pragma unroll
-                    for (int qq = 0; qq < 4; qq++)
-                        kn[qq] = (uint32_t)row[b[qq]] | ((uint32_t)row[b[qq + 4]] << 16);
+                    for (int qq = 0; qq < 4; qq++) {  // lo + hi * 65536 on the FMA pipe (IMAD), not PRMT
+                        uint32_t w;
+                        asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(w) : "r"((uint32_t)row[b[qq + 4]]),
+                            "r"((uint32_t)row[b[qq]]));
+                        kn[qq] = w;
+                    }
                 });
                 const double v = __ldg(a.vals + L);
                 e0 = i == 0 ? v : e0;
@@ -182,10 +199,8 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         char* blocks = sets + (size_t)set * kE8SetBytes;
 #pragma unroll
         for (int i = 0; i < 4; i++) {
-            const int t = lane + 32 * i;
-            if (t < 112) {
-                const int cc = t / 28, pi = t - cc * 28;
-                double* dst = reinterpret_cast<double*>(blocks) + cc * kHK8Block + eslot[pi];
+            if (job[i]) {
+                double* dst = reinterpret_cast<double*>(blocks) + (job[i] >> 16);
                 dst[0] = e[i];  // h[{j, j2}][j] and h[{j, j2}][j2]
                 dst[kHK8EdgeStride] = e[i];
             }
