@@ -272,6 +272,26 @@ def run_ours():
     t_ms = float(tt.item())
     value = P * ARGS.steps * world / (t_ms / 1000.0)
 
+    # the same pricing with the stage order reconstructed (comm_cost's
+    # PathResult; the compact-table warp kernel), reported beside the headline
+    order_out = torch.empty((P, 8), dtype=torch.int8, device=dev)
+    pg_out = torch.empty((P, 8), dtype=torch.float64, device=dev)
+
+    def order_step(i):
+        N.check(L.hs_eval_batch(inst.handle, pops[i % nbuf].data_ptr(), P, outs[0].data_ptr(), outs[1].data_ptr(),
+                                outs[2].data_ptr(), pg_out.data_ptr(), order_out.data_ptr(), bad.data_ptr(), sp),
+                "hs_eval_batch(order)")
+
+    order_step(0)
+    barrier()
+    oa, ob = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    oa.record(stream)
+    for i in range(3):
+        order_step(i)
+    ob.record(stream)
+    barrier()
+    order_rate = P * 3 / (oa.elapsed_time(ob) / 1000.0)
+
     # e2e through the C-ABI host-buffer entry point: pinned host layouts in,
     # totals/datap/pipelinep out, H2D/D2H inside the timed region.
     host_pop = [pops[i].cpu().pin_memory().numpy() for i in range(2)]
@@ -304,7 +324,10 @@ def run_ours():
     kern_ms = sum(launch_ms) / len(launch_ms)
     achieved = SMEM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = SMEM_BYTES_PER_CLK_SM * sms * sm_mhz * 1e6 / 1e9
+    arch_peak = SMEM_BYTES_PER_CLK_SM * sms * sm_mhz * 1e6 / 1e9
+    # measured denominator: conflict-free LDS.128 stream on every SM (hs_probe.cu)
+    measured_peak = N.smem_bandwidth(local) / 1e9
+    peak = measured_peak
     traffic, traffic_src, smem_wf, pipes = None, None, None, None
     tp = ROOT / "profiles" / "eval_traffic.json"
     if tp.exists():  # ncu --set full capture of this kernel (scripts/gpu_ncu.sh)
@@ -329,12 +352,17 @@ def run_ours():
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
                      "smem_wavefront_bytes": smem_wf, "pipes": pipes,
-                     "per_eval_bytes": SMEM_BYTES_PER_EVAL, "kernel": "eval_warp_kernel", "kernel_ms": kern_ms,
-                     "peak_source": f"architectural 128 B/clk/SM x {sms} SMs at the {sm_mhz:.0f} MHz SM clock "
-                                    "sampled during this run (MEASURED_PEAKS.json has no smem figure)",
+                     "per_eval_bytes": SMEM_BYTES_PER_EVAL, "kernel": "hs::eval8_kernel", "kernel_ms": kern_ms,
+                     "peak_source": "measured in this run: hs_probe_smem_bandwidth (conflict-free 16-byte LDS on "
+                                    f"all {sms} SMs; MEASURED_PEAKS.json has no shared-memory figure); architectural "
+                                    f"128 B/clk/SM at the sampled {sm_mhz:.0f} MHz = {arch_peak:.0f} GB/s",
+                     "arch_peak": arch_peak,
                      "hbm_achieved_gbs": HBM_BYTES_PER_EVAL * P / (kern_ms / 1000.0) / 1e9},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": P * 128, "d2h_bytes_per_step": P * 24,
                 "path": "hs_eval_batch_host (C-ABI, pinned host buffers)"},
+        "with_stage_order": {"value": order_rate, "unit": "evals/s",
+                             "what": "same workload with per_group + pipeline order (comm_cost's full CostBreakdown; "
+                                     "eval_warp_kernel, compact Held-Karp table), device-resident, 3 launches"},
         "gpu_launches": ARGS.steps,
         "clocks": {"sm_mhz": csum["sm_mhz"], "sm_max_mhz": csum["sm_max_mhz"], "reasons": csum["reasons"]},
     }

@@ -36,6 +36,11 @@ typedef struct {
 
 int hs_version(void);
 const char *hs_last_error(void);
+/* Measurement helper (no reference counterpart): shared-memory bandwidth of
+ * `device` in bytes/s over all SMs (conflict-free 16-byte loads), the
+ * measured denominator of bench.py's on-chip roofline; *ms (optional) is
+ * one probe launch. */
+int hs_probe_smem_bandwidth(int device, double *bytes_per_s, double *ms);
 
 /* One network instance + workload on one device: uploads lat/bw (n*n
  * float64, symmetric, bw diagonal +inf) and builds the DP/PP/SW pair tables

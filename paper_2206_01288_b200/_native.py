@@ -162,6 +162,7 @@ def lib():
         L.hs_datap_group_batch.argtypes = [vp, vp, i32, i64, dbl, dbl, vp, i32, vp]
         L.hs_brute_force.argtypes = [vp, i32, i32, vp, vp, i32, vp]
         L.hs_unrank_partitions.argtypes = [i32, i32, i32, i64, i64, vp, vp]
+        L.hs_probe_smem_bandwidth.argtypes = [i32, vp, vp]
         for name in EXPORTS:
             if name not in ("hs_version", "hs_last_error"):
                 getattr(L, name).restype = i32
@@ -176,7 +177,14 @@ EXPORTS = ("hs_version", "hs_last_error", "hs_instance_create", "hs_instance_des
            "hs_ga_export", "hs_ga_import", "hs_ga_result", "hs_ga_destroy", "hs_local_search", "hs_refine_pass",
            "hs_crossover", "hs_gains", "hs_random_partitions", "hs_materialize", "hs_evaluate_assignments",
            "hs_random_assignments", "hs_count_partitions", "hs_unrank_partitions", "hs_bottleneck_match_batch",
-           "hs_datap_group_batch", "hs_brute_force")
+           "hs_datap_group_batch", "hs_brute_force", "hs_probe_smem_bandwidth")
+
+
+def smem_bandwidth(device: int = 0) -> float:
+    """Measured shared-memory bandwidth of the GPU, bytes/s (hs_probe.cu)."""
+    out = np.zeros(2)
+    check(lib().hs_probe_smem_bandwidth(device, out.ctypes.data, out[1:].ctypes.data), "hs_probe_smem_bandwidth")
+    return float(out[0])
 
 
 def check(rc: int, what: str) -> None:

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
                 Es[rr * kES16 + cc] = src[(size_t)rr * es + cc];
             }
         }
+        HS_JITTER();
         __syncthreads();
         cl.sync();  // every reader of the previous candidate is done
         if (!skip) {
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
                 double* const* dst = rb[p & 1];
                 const int Cin = t.C[p - 1];
                 const int end = t.rbeg[p][rank + 1];
+                HS_JITTER();
                 for (int x = t.rbeg[p][rank] + (int)threadIdx.x; x < end; x += blockDim.x) {
                     const uint64_t rw = __ldg(t.rwords + x);
                     switch (p) {
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const doubl
                         default: two_source<15>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
                     }
                 }
+                HS_JITTER();
                 cl.sync();
             }
             if (rank == 0 && threadIdx.x == 0) {  // layer k: the full set's k entries, slots 0..k-1

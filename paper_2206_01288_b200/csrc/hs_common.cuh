@@ -15,6 +15,26 @@ namespace hs {
 constexpr int kWarp = 32;
 constexpr double kInf = __builtin_huge_val();
 
+// Race stress (compute-sanitizer is unavailable on the GPU pool): a build
+// with -DHS_RACE_JITTER sleeps a pseudo-random 0..2 us per thread at the
+// cross-warp / cross-CTA hand-off points (HS_JITTER()), so a missing
+// barrier or fence shows up as a parity failure against the oracle
+// (scripts/race_stress.sh).  Compiles to nothing otherwise.
+#ifdef HS_RACE_JITTER
+__device__ __forceinline__ void hs_jitter() {
+    unsigned x = (unsigned)clock() ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu);
+    x ^= x >> 13;
+    x *= 0x5bd1e995u;
+    x ^= x >> 15;
+    __nanosleep(x & 2047u);
+}
+#define HS_JITTER() ::hs::hs_jitter()
+#else
+#define HS_JITTER() \
+    do {            \
+    } while (0)
+#endif
+
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 __device__ __forceinline__ double dmax(double a, double b) { return b > a ? b : a; }
 

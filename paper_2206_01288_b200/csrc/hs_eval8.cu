@@ -27,6 +27,7 @@
 // 227 KB of shared memory allowed with one private set per warp.
 #include "hs_hk8_gen.cuh"
 #include "hs_match8_dp.cuh"
+#include "hs_tma.cuh"
 #include "hs_warp_eval.cuh"
 
 namespace hs {
@@ -35,8 +36,18 @@ namespace hs {
 #define HS_E8_WARPS 16
 #endif
 constexpr int kE8Warps = HS_E8_WARPS;
-constexpr int kE8DS = 65;  // DP row stride (doubles)
+#ifndef HS_E8_TMA
+#define HS_E8_TMA 1
+#endif
+#if HS_E8_TMA
+// rows staged by bulk copies (16-byte aligned destinations): strides of
+// 132 and 36 words, 4 banks apart row to row
+constexpr int kE8DS = 66;  // DP row stride (doubles)
+constexpr int kE8RS = 72;  // rank row stride (u16)
+#else
+constexpr int kE8DS = 65;  // DP row stride (doubles): odd word count
 constexpr int kE8RS = 66;  // rank row stride (u16): 33 words, odd
+#endif
 constexpr size_t kE8OffBytes = (size_t)8 * kHK8Words * 4 + 64;  // + layer-2 edge slots
 constexpr size_t kE8RkBytes = ((size_t)64 * kE8RS * 2 + 15) & ~(size_t)15;
 constexpr size_t kE8DpBytes = (size_t)64 * kE8DS * 8;
@@ -66,6 +77,31 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
     char* sets = reinterpret_cast<char*>(memsm + kE8Warps * kE8MemBytes + 16);
     const uint16_t* grk = reinterpret_cast<const uint16_t*>(a.rank);
     uint16_t* eslot = reinterpret_cast<uint16_t*>(offs + 8 * kHK8Words);
+#if HS_E8_TMA
+    // tables by the bulk-copy (TMA) engine: warp 0 arms one mbarrier with the
+    // byte count and issues 129 row copies (Held-Karp offsets, 64 rank rows,
+    // 64 DP rows); the other threads set up the rest meanwhile
+    __shared__ __align__(8) uint64_t tbar;
+    if (threadIdx.x == 0) mbar_init(&tbar, 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        constexpr uint32_t kOffs = 8 * kHK8Words * 4;
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&tbar, kOffs + 64 * 128 + 64 * 512);
+        __syncwarp();
+        for (int i = threadIdx.x; i < 129; i += 32) {
+            if (i < 64)
+                bulk_g2s(rk + i * kE8RS, grk + i * 64, 128, &tbar);
+            else if (i < 128)
+                bulk_g2s(dp + (i - 64) * kE8DS, a.dp + (i - 64) * 64, 512, &tbar);
+            else
+                bulk_g2s(offs, kHK8Offs, kOffs, &tbar);
+        }
+    }
+    if (threadIdx.x >= 32 && threadIdx.x < 60) eslot[threadIdx.x - 32] = kHK8Edge[threadIdx.x - 32];
+    if (threadIdx.x == 64) *freemask = kE8Sets == 32 ? 0xffffffffu : (1u << kE8Sets) - 1u;
+    mbar_wait(&tbar, 0);
+    __syncthreads();
+#else
     for (int i = threadIdx.x; i < 8 * kHK8Words; i += blockDim.x) offs[i] = kHK8Offs[i];
     if (threadIdx.x < 28) eslot[threadIdx.x] = kHK8Edge[threadIdx.x];
     if (threadIdx.x == 0) *freemask = kE8Sets == 32 ? 0xffffffffu : (1u << kE8Sets) - 1u;
@@ -75,6 +111,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         dp[r * kE8DS + c] = a.dp[i];
     }
     __syncthreads();
+#endif
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int c = lane >> 3, g = lane & 7;
@@ -179,6 +216,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         }
         const double e[4] = {e0, e1, e2, e3};
         // take a free Held-Karp set
+        HS_JITTER();
         int set = 0;
         if (lane == 0) {
             unsigned old = *reinterpret_cast<volatile unsigned*>(freemask);
@@ -205,8 +243,10 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
                 dst[kHK8EdgeStride] = e[i];
             }
         }
+        HS_JITTER();
         __syncwarp();
         double pipe = hk8_lane(blocks + (size_t)c * kHK8Block * 8, t4);
+        HS_JITTER();
         __syncwarp();  // every lane is done with the set
         if (lane == 0) {
             __threadfence_block();

@@ -613,8 +613,10 @@ static __device__ bool pass_sweep_waves(LS& s, Pcg64& rng, int wid, int lane, in
         for (int x = wstart[w] + wid; x < wstart[w + 1]; x += W) {
             int j, j2;
             decode_pair(order[x], k, j, j2);
+            HS_JITTER();
             if (sweep_pair8<kSh, true>(s, j, j2, lane, pi, pl) && lane == 0) atomicOr(flag, 1);
         }
+        HS_JITTER();
         __syncthreads();
     }
     return *flag != 0;
@@ -1491,6 +1493,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int isl = kWI ? blockIdx.x * W + wid : blockIdx.x;
     auto island_sync = [&]() {
+        HS_JITTER();
         if constexpr (kWI)
             __syncwarp();
         else

@@ -270,7 +270,7 @@ constexpr int kHK8EdgeStride = {NP[2]};  // doubles between the two copies of an
 constexpr int kHK8Words = {WORDS};     // offset words per end vertex
 
 // [u][kHK8Words]: E[u][v] offsets (7), then read | write << 16 per state
-__device__ const uint32_t kHK8Offs[{K} * {WORDS}] = {{
+__device__ __align__(16) const uint32_t kHK8Offs[{K} * {WORDS}] = {{
 {flat}
 }};
 

@@ -112,7 +112,7 @@ if os.path.exists(rp):
                   "| reason | ratio |", "|---|---:|"]
         lines += [f"| {n} | {v:.3f} |" for v, n in sorted(st, reverse=True)]
         lines.append("")
-        if "eval_warp_kernel" in name and os.environ.get("POP"):
+        if ("eval_warp_kernel" in name or "eval8_kernel" in name) and os.environ.get("POP"):
             # per-launch DRAM traffic of the fitness kernel, read by bench.py
             # for roofline.traffic (bytes per launch at population POP)
             def num(key, scale):
