@@ -66,6 +66,8 @@ struct hs_ga {
     double* hk_scratch = nullptr;
     long long* prof = nullptr;  // HS_GA_PROFILE=1: driver-phase cycle counters of island 0
     cudaStream_t last = nullptr;  // stream of the latest run / export / import (hs_ga_result syncs it)
+    int spec = -1;                // speculative pipeline cluster size (0: off, -1: not probed yet)
+    bool started = false;         // the population has been initialised by a launch
 };
 
 static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
@@ -160,10 +162,34 @@ int hs_ga_run(hs_ga* ga, int until, void* stream) {
     DeviceGuard dg(ga->h->device);
     if (int rc_ = hsx::ensure_search_stack()) return rc_;
     until = std::min(until, ga->cfg.generations);
-    hs::GAArgs a = ga_args(ga, until, until >= ga->cfg.generations);
-    if (hs::launch_ga(a, ga->plan, ga->islands, ga->h->rank16 != nullptr, (cudaStream_t)stream))
-        return fail(-1, "ga launch", cudaGetLastError());
-    ga->last = (cudaStream_t)stream;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool key16 = ga->h->rank16 != nullptr;
+    if (ga->spec < 0) {
+        // one GA: generations as a speculative pipeline over a thread-block
+        // cluster (hs_search_ga_spec.cu); HS_GA_SPEC=0 keeps the one-CTA kernel
+        const char* env = getenv("HS_GA_SPEC");
+        const bool want = ga->islands == 1 && !ga->prof && !(env && env[0] == '0');
+        ga->spec = want ? hs::ga_spec_cluster(ga_args(ga, until, 0), ga->plan, key16, ga->h->smem_optin) : 0;
+        cudaGetLastError();
+    }
+    if (ga->spec > 1) {
+        if (!ga->started) {  // init_population + pricing (no generation runs)
+            hs::GAArgs a0 = ga_args(ga, 0, 0);
+            if (hs::launch_ga(a0, ga->plan, 1, key16, st)) return fail(-1, "ga init launch", cudaGetLastError());
+        }
+        hs::GAArgs a = ga_args(ga, until, 0);
+        if (hs::launch_ga_spec(a, ga->plan, ga->spec, key16, st))
+            return fail(-1, "ga speculative launch", cudaGetLastError());
+        if (until >= ga->cfg.generations) {  // finalize (no generation left to run)
+            hs::GAArgs af = ga_args(ga, until, 1);
+            if (hs::launch_ga(af, ga->plan, 1, key16, st)) return fail(-1, "ga finalize launch", cudaGetLastError());
+        }
+    } else {
+        hs::GAArgs a = ga_args(ga, until, until >= ga->cfg.generations);
+        if (hs::launch_ga(a, ga->plan, ga->islands, key16, st)) return fail(-1, "ga launch", cudaGetLastError());
+    }
+    ga->started = true;
+    ga->last = st;
     return 0;
 }
 

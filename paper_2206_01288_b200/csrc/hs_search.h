@@ -88,6 +88,10 @@ struct SearchPlan {
 
 int search_plan(const SearchShape& sh, int P, size_t smem_optin, SearchPlan* plan, bool warp_islands = false);
 int launch_ga(const GAArgs& a, const SearchPlan& plan, int islands, bool key16, cudaStream_t st);
+// one GA as a speculative generation pipeline over a thread-block cluster
+// (hs_search_ga_spec.cu): cluster size for this plan (0 = unavailable), launch
+int ga_spec_cluster(const GAArgs& a, const SearchPlan& plan, bool key16, size_t smem_optin);
+int launch_ga_spec(const GAArgs& a, const SearchPlan& plan, int cluster, bool key16, cudaStream_t st);
 int launch_refine(const RefineArgs& a, const SearchPlan& plan, int B, bool key16, cudaStream_t st);
 int launch_crossover(int n, int k, int m, const int16_t* p1, const int16_t* p2, hs_pcg64* rngs, int16_t* out, int B,
                      cudaStream_t st);
