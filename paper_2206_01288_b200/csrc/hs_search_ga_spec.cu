@@ -17,13 +17,17 @@
 // shared memory.  Workers run the unchanged refine / pricing code (sweep
 // waves over their 8 warps, register chain rounds, warp pricing) and post
 // the best snapshot back.  The sequencer commits generations strictly in
-// order with the reference's selection rules; a job is only issued when
-// neither parent can be replaced by a generation still in flight (the f
-// in-flight generations can only replace the f costliest members, first
-// maximum first), and a wrong sweep-count prediction or a patience stop
-// discards every later in-flight job and re-issues from the committed
-// stream.  Results, traces, evaluation counts and the final stream state
-// are therefore exactly those of the sequential kernel.
+// order with the reference's selection rules.  Two things can invalidate a
+// job already in flight, and both are checked at commit: a wrong sweep-count
+// prediction for the committing generation (every later job started from a
+// wrong stream position), and a replacement of a member that a later job
+// took as a parent (that job and every later one: their crossover draws
+// depend on the parents).  Replacements are rare (6% of the generations of
+// the 1000-generation anchors), so jobs are issued optimistically; the
+// invalid ones are drained and re-issued from the recorded stream state.
+// A patience stop drains everything after it.  Results, traces, evaluation
+// counts and the final stream state are exactly those of the sequential
+// kernel.
 #include <cooperative_groups.h>
 
 #include "hs_search_impl.cuh"
@@ -63,6 +67,45 @@ __device__ __forceinline__ int ld_acquire_cluster(const int* p) {
 }
 
 __device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+
+// The stream consumption of crossover(p1, p2, rng) (scheduler.py:139-174)
+// without building the child: the draws depend on the parents only through
+// the number of differing slots, the chosen slot's |diff| and the drawn
+// subset size.  Same calls, same order as crossover() (hs_search_impl.cuh).
+__device__ __noinline__ void crossover_draws(LS& s, const int16_t* p1, const int16_t* p2, Pcg64& rng, int lane) {
+    const int k = s.k, m = s.m;
+    for (int t = lane; t < k * m; t += kWarp) s.grp_of[p1[t]] = (int8_t)(t / m);
+    __syncwarp();
+    // lane j < k: |diff_j| = members of p2's group j outside p1's group j
+    int c = 0;
+    if (lane < k)
+        for (int i = 0; i < m; i++) c += s.grp_of[p2[lane * m + i]] != lane;
+    const unsigned nz = __ballot_sync(kFull, lane < k && c > 0);
+    int cnts[16];
+#pragma unroll
+    for (int j = 0; j < 16; j++) cnts[j] = __shfl_sync(kFull, c, j);
+    if (lane == 0) {
+        const int ns = __popc(nz);
+        if (ns > 0) {
+            const int pick = (int)rng.integers(0, ns);
+            int j = 0;
+            for (unsigned b = nz, q = 0;; b &= b - 1, q++) {
+                if ((int)q == pick) {
+                    j = __ffs(b) - 1;
+                    break;
+                }
+            }
+            int nd = 0;
+#pragma unroll
+            for (int x = 0; x < 16; x++) nd = x == j ? cnts[x] : nd;
+            const int mi = (int)rng.integers(1, nd + 1);
+            for (int jj = nd - mi; jj < nd; jj++) (void)rng.bounded((uint64_t)jj);  // Floyd
+            for (int i = mi - 1; i >= 1; i--) (void)rng.bounded((uint64_t)i);       // shuffle
+            for (int t = 0; t < mi; t++) (void)rng.integers(0, m - t);              // evictions
+        }
+    }
+    __syncwarp();
+}
 
 template <bool kSmemTables, typename KeyT, bool kM8>
 __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl) {
@@ -148,10 +191,13 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
             hs_pcg64 rcommit = st.rng;  // stream after the last committed generation
             int pred = (a.kind == 0 && m >= 2) ? (a.max_passes + 1) / 2 : 0;
             int gen_c = st.gen, gen_s = st.gen, seqctr = 0;
-            bool stopping = st.stopped != 0, blocked = false;
+            bool stopping = st.stopped != 0;
             int wseq[kSpecMaxCluster], wstate[kSpecMaxCluster];  // state: 0 free, 1 live job, 2 draining
-            int ring[kSpecMaxCluster], assumed[kSpecMaxCluster];  // per in-flight generation (gen % 16)
-            for (int x = 0; x < kSpecMaxCluster; x++) wseq[x] = wstate[x] = ring[x] = assumed[x] = 0;
+            // per in-flight generation (index gen % 16): worker, predicted sweep
+            // draws, parent slots, stream state before its parent draws
+            int ring[kSpecMaxCluster], assumed[kSpecMaxCluster], par1[kSpecMaxCluster], par2[kSpecMaxCluster];
+            hs_pcg64 start[kSpecMaxCluster];
+            for (int x = 0; x < kSpecMaxCluster; x++) wseq[x] = wstate[x] = ring[x] = assumed[x] = par1[x] = par2[x] = 0;
             for (;;) {
                 int act = 0, w = -1;
                 if (lane == 0) {
@@ -169,7 +215,7 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
                             bool idle = gen_c == gen_s;
                             for (int x = 0; x < NW; x++) idle = idle && wstate[x] == 0;
                             if (idle) act = 3;
-                        } else if (!blocked && gen_s < gen_end && gen_s - gen_c < NW) {
+                        } else if (gen_s < gen_end && gen_s - gen_c < NW) {
                             for (int x = 0; x < NW && w < 0; x++)
                                 if (wstate[x] == 0) w = x;
                             if (w >= 0) act = 2;
@@ -214,15 +260,24 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
                             st.stopped = 1;
                             stopping = true;
                         }
+                        // first later in-flight job that is no longer valid
+                        int bad = gen_s;
                         if (mispredicted || stopping) {
-                            // every later in-flight job started from a wrong stream
-                            // position (or is past the stop): drain and re-issue
-                            for (int q = gen_c; q < gen_s; q++) wstate[ring[q % kSpecMaxCluster]] = 2;
-                            gen_s = gen_c;
-                            rs.load(rcommit);
+                            bad = gen_c;  // wrong stream position for all of them / past the stop
+                        } else if (replace) {
+                            for (int q = gen_c; q < gen_s && bad == gen_s; q++)
+                                if (par1[q % kSpecMaxCluster] == worst || par2[q % kSpecMaxCluster] == worst) bad = q;
+                        }
+                        if (bad < gen_s) {  // drain those jobs, re-issue from `bad`
+                            for (int q = bad; q < gen_s; q++) wstate[ring[q % kSpecMaxCluster]] = 2;
+                            if (bad == gen_c) {
+                                rs.load(rcommit);
+                            } else {
+                                rs.load(start[bad % kSpecMaxCluster]);
+                            }
+                            gen_s = bad;
                             if (mispredicted) pred = R.draws;
                         }
-                        blocked = false;
                     }
                     worst = __shfl_sync(kFull, worst, 0);
                     replace = __shfl_sync(kFull, replace, 0);
@@ -232,36 +287,27 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
                     __syncwarp();
                     continue;
                 }
-                // act == 2: issue generation gen_s on worker w
-                int i = 0, i2 = 0, risk = 0;
+                // act == 2: issue generation gen_s on worker w (parents from the
+                // committed population; checked against later replacements at commit)
+                int i = 0, i2 = 0;
                 Pcg64 t = rs;
                 hs_pcg64 after_parents;
                 if (lane == 0) {
+                    t.store(start[gen_s % kSpecMaxCluster]);
                     i = (int)t.integers(0, P);
                     i2 = (int)t.integers(0, P - 1);
                     if (i2 >= i) i2++;
                     t.store(after_parents);
-                    // the f in-flight generations can only replace the f costliest
-                    // members (by cost, then index: the first maximum goes first)
-                    const int f = gen_s - gen_c;
-                    int ri = 0, ri2 = 0;
-                    for (int q = 0; q < P; q++) {
-                        const double c = g.popcost[q];
-                        ri += c > g.popcost[i] || (c == g.popcost[i] && q < i);
-                        ri2 += c > g.popcost[i2] || (c == g.popcost[i2] && q < i2);
-                    }
-                    risk = ri < f || ri2 < f;
-                    if (risk) blocked = true;  // retry after the next commit
+                    par1[gen_s % kSpecMaxCluster] = i;
+                    par2[gen_s % kSpecMaxCluster] = i2;
                 }
-                risk = __shfl_sync(kFull, risk, 0);
-                if (risk) continue;
                 i = __shfl_sync(kFull, i, 0);
                 i2 = __shfl_sync(kFull, i2, 0);
                 copy16(g.par, pop + (size_t)i * km, km, lane);
                 copy16(g.par + km, pop + (size_t)i2 * km, km, lane);
                 __syncwarp();
-                // replay the crossover for its stream consumption (depends on the parents)
-                crossover(s, g.par, g.par + km, t, g.snaps, lane);
+                // the crossover's stream consumption (depends on the parents)
+                crossover_draws(s, g.par, g.par + km, t, lane);
                 SpecJob* jw = cl.map_shared_rank(job, w + 1);
                 for (int q = lane; q < 2 * km; q += kWarp) jw->par[q] = g.par[q];
                 if (lane == 0) {

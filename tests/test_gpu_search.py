@@ -337,3 +337,31 @@ def test_ga_session_results_sync_and_partial_run_errors():
         sess.results()
     sess.run(40, stream=side.cuda_stream)  # no host synchronisation before results()
     assert sess.results()[0].to_dict() == one.to_dict()
+
+
+@pytest.mark.parametrize("name,kind,pop,gens,patience,max_passes",
+                         [("case5", "ours", 16, 120, None, 8), ("case2", "ours", 64, 80, None, 8),
+                          ("case4", "ours", 32, 150, 6, 8), ("case3", "kl", 24, 90, None, 8),
+                          ("case1", "none", 16, 70, 9, 8), ("r24_3x8", "ours", 12, 60, None, 5),
+                          ("r16_4x4", "ours", 20, 60, 4, 3), ("config1", "ours", 64, 100, None, 8)])
+def test_speculative_pipeline_equals_oracle(name, kind, pop, gens, patience, max_passes):
+    """One evolve runs as the speculative cluster pipeline (hs_search_ga_spec.cu):
+    stream-position mispredictions (case 2: two sweep passes, predicted
+    four), parent replacements under in-flight jobs, patience stops and
+    epoch boundaries must leave the trace, result, evaluations and the
+    caller's stream exactly those of the oracle."""
+    g, w = I.instance(name)
+    cfg = S.ScheduleConfig(pop_size=pop, generations=gens, local_search=kind, seed=11, patience=patience,
+                           max_passes=max_passes)
+    o = O.Oracle.of(g, w).evolve(pop, gens, kind, seed=11, max_passes=max_passes, patience=patience)
+    r = S.evolve(g, w, cfg)
+    assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+    assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+    assert [t[1] for t in r.trace] == list(o["trace_best"])
+    assert [t[2] for t in r.trace] == list(o["trace_mean"])
+    # the same run in epochs (several launches of the pipeline)
+    rng = np.random.Generator(np.random.PCG64(11))
+    sess = S.GASession(g, w, cfg, [rng])
+    for until in (gens // 3, gens // 2, gens):
+        sess.run(until)
+    assert sess.results()[0].to_dict() == r.to_dict()
