@@ -93,8 +93,30 @@ __global__ void __launch_bounds__(128) stage_kernel(EvalArgs a, double* __restri
     }
 }
 
+// min over NV values as a balanced tree (the value of a min of doubles does
+// not depend on the order; a short dependency chain instead of NV - 1)
+template <int NV>
+__device__ __forceinline__ double tree_min(const double (&c)[NV]) {
+    double x[NV];
+#pragma unroll
+    for (int i = 0; i < NV; i++) x[i] = c[i];
+#pragma unroll
+    for (int w = 1; w < NV; w *= 2)
+#pragma unroll
+        for (int i = 0; i + w < NV; i += 2 * w) x[i] = x[i + w] < x[i] ? x[i + w] : x[i];
+    return x[0];
+}
+
+// HS_HK_ILP=1: two tasks per iteration with min trees (needs ~100 registers,
+// so one CTA per SM); measured slower than two 64-register CTAs per SM
+#ifndef HS_HK_ILP
+#define HS_HK_ILP 0
+#endif
+#if HS_HK_ILP
 // One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
-// w[.][v] for v in r stay in registers while every u not in r is relaxed.
+// w[.][v] for v in r stay in registers while every u not in r is relaxed,
+// two u at a time (independent loads / adds / min trees for ILP; one CTA
+// per SM leaves 128 registers per thread).
 template <int NV>
 __device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
                                            uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
@@ -104,32 +126,81 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
     const bool straddle = (rw >> 33) & 1;
     const uint32_t* dw = dwords + (rw >> 34);
     double hv[NV];
-    uint32_t voff[NV];
+    const char* ev[NV];  // &w[0][v]
 #pragma unroll
     for (int i = 0; i < NV; i++) {
         const int v = __ffs(r) - 1;
         r &= r - 1;
-        voff[i] = (uint32_t)v * 8u;
+        ev[i] = reinterpret_cast<const char*>(Es) + v * 8;
         const int li = lr + i;
         hv[i] = (!straddle || li < Cin) ? own[li] : next[li - Cin];
     }
     uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
-    uint32_t dn = __ldg(dw);
-    for (int j = 0; rest; j++) {
-        const int u = __ffs(rest) - 1;
+    for (int j = 0; rest; j += 2) {
+        const int u0 = __ffs(rest) - 1;
         rest &= rest - 1;
-        const uint32_t d = dn;
-        if (rest) dn = __ldg(dw + j + 1);
-        const char* Eu = reinterpret_cast<const char*>(Es + u * kES16);
-        double best = kInf;
+        const bool two = rest != 0;
+        const int u1 = two ? __ffs(rest) - 1 : u0;
+        rest &= rest - 1;
+        const uint32_t d0 = __ldg(dw + j);
+        const uint32_t d1 = two ? __ldg(dw + j + 1) : 0u;
+        const int o0 = u0 * kES16 * 8, o1 = u1 * kES16 * 8;
+        double c0[NV], c1[NV];
 #pragma unroll
         for (int i = 0; i < NV; i++) {
-            const double c = *reinterpret_cast<const double*>(Eu + voff[i]) + hv[i];
-            best = c < best ? c : best;
+            c0[i] = *reinterpret_cast<const double*>(ev[i] + o0) + hv[i];
+            c1[i] = *reinterpret_cast<const double*>(ev[i] + o1) + hv[i];
         }
-        dst[d >> 17][d & 0x1FFFF] = best;
+        dst[d0 >> 17][d0 & 0x1FFFF] = tree_min<NV>(c0);
+        if (two) dst[d1 >> 17][d1 & 0x1FFFF] = tree_min<NV>(c1);
     }
 }
+
+#else
+// One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
+// w[.][v] for v in r stay in registers while every u not in r is relaxed,
+// two u at a time (independent loads / adds / min trees for ILP; one CTA
+// per SM leaves 128 registers per thread).
+template <int NV>
+__device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
+                                           uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
+                                           double* const* dst) {
+    uint32_t r = (uint32_t)(rw & 0xFFFF);
+    const int lr = (int)(rw >> 16) & 0x1FFFF;
+    const bool straddle = (rw >> 33) & 1;
+    const uint32_t* dw = dwords + (rw >> 34);
+    double hv[NV];
+    const char* ev[NV];  // &w[0][v]
+#pragma unroll
+    for (int i = 0; i < NV; i++) {
+        const int v = __ffs(r) - 1;
+        r &= r - 1;
+        ev[i] = reinterpret_cast<const char*>(Es) + v * 8;
+        const int li = lr + i;
+        hv[i] = (!straddle || li < Cin) ? own[li] : next[li - Cin];
+    }
+    uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
+    for (int j = 0; rest; j += 2) {
+        const int u0 = __ffs(rest) - 1;
+        rest &= rest - 1;
+        const bool two = rest != 0;
+        const int u1 = two ? __ffs(rest) - 1 : u0;
+        rest &= rest - 1;
+        const uint32_t d0 = __ldg(dw + j);
+        const uint32_t d1 = two ? __ldg(dw + j + 1) : 0u;
+        const int o0 = u0 * kES16 * 8, o1 = u1 * kES16 * 8;
+        double c0[NV], c1[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            c0[i] = *reinterpret_cast<const double*>(ev[i] + o0) + hv[i];
+            c1[i] = *reinterpret_cast<const double*>(ev[i] + o1) + hv[i];
+        }
+        dst[d0 >> 17][d0 & 0x1FFFF] = tree_min<NV>(c0);
+        if (two) dst[d1 >> 17][d1 & 0x1FFFF] = tree_min<NV>(c1);
+    }
+}
+
+#endif
 
 // layer 2: r = {v}, h[r][v] = 0 (implicit): h[{u, v}][u] = w[u][v]
 __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, uint32_t full,
@@ -146,7 +217,12 @@ __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, 
     }
 }
 
-__global__ void __launch_bounds__(kClusterThreads) hk_cluster_kernel(const double* __restrict__ E, int es,
+// two 512-thread CTAs per SM (64 registers): 16-CTA clusters cover 8 SMs,
+// 18 co-resident clusters instead of 7 (config 4: 122k -> 141k evals/s)
+#ifndef HS_HK_MINB
+#define HS_HK_MINB 2
+#endif
+__global__ void __launch_bounds__(kClusterThreads, HS_HK_MINB) hk_cluster_kernel(const double* __restrict__ E, int es,
                                                                      int64_t estride, int k, int64_t B, HKTwo t,
                                                                      const double* __restrict__ add,
                                                                      const uint8_t* __restrict__ bad,

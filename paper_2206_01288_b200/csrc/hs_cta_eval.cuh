@@ -117,10 +117,16 @@ struct CtaScratch {
     double* E;     // 16 x 17
     double* pg;    // 16
     double* red;   // 2
+    uint32_t* wk;  // kMatchWarps key blocks of m x (m | 1) (warp_bottleneck; unused by the 8 x 8 u16 path)
 };
 
+constexpr int kMatchWarps = 4;  // warps of a CTA that solve the m != 8 bottleneck matchings
+
+__host__ __device__ inline size_t cta_wkeys_bytes(int m, int warps) { return (size_t)warps * m * (m | 1) * 4; }
+
 __host__ __device__ inline size_t cta_scratch_bytes(int k, int m) {
-    return ((size_t)k * m * 8 + 15) / 16 * 16 + 16 * kES16 * 8 + 16 * 8 + 16;
+    return ((size_t)k * m * 8 + 15) / 16 * 16 + 16 * kES16 * 8 + 16 * 8 + 16 +
+           (cta_wkeys_bytes(m, kMatchWarps) + 15) / 16 * 16;
 }
 
 __device__ inline CtaScratch cta_scratch_at(unsigned char* base, int k, int m) {
@@ -132,6 +138,8 @@ __device__ inline CtaScratch cta_scratch_at(unsigned char* base, int k, int m) {
     c.pg = reinterpret_cast<double*>(base);
     base += 16 * 8;
     c.red = reinterpret_cast<double*>(base);
+    base += 16;
+    c.wk = reinterpret_cast<uint32_t*>(base);
     return c;
 }
 
@@ -157,25 +165,45 @@ __device__ inline double cta_stage(int n, int k, int m_rt, const double* DP, con
         cs.pg[threadIdx.x] = mx;
     }
     const int npairs = k * (k - 1) / 2;
-    for (int tt = threadIdx.x; tt < npairs; tt += blockDim.x) {
-        int j, j2;
-        decode_pair(tt, k, j, j2);
-        const int16_t* A = mem + j * m;
-        const int16_t* B = mem + j2 * m;
-        uint32_t L;
-        if (kM8) {
-            L = match8_dp([&](int r, uint32_t(&kn)[4]) {
+    if (kM8) {  // one thread per pair: the branch-free 8 x 8 subset DP
+        for (int tt = threadIdx.x; tt < npairs; tt += blockDim.x) {
+            int j, j2;
+            decode_pair(tt, k, j, j2);
+            const int16_t* A = mem + j * m;
+            const int16_t* B = mem + j2 * m;
+            const uint32_t L = match8_dp([&](int r, uint32_t(&kn)[4]) {
                 const KeyT* row = RK + (size_t)A[r] * rs;
 #pragma unroll
                 for (int q = 0; q < 4; q++) kn[q] = (uint32_t)row[B[q]] | ((uint32_t)row[B[q + 4]] << 16);
             });
-        } else {
-            L = bottleneck_threshold<uint32_t>(
-                m, [&](int r, int c) { return (uint32_t)RK[(size_t)A[r] * rs + B[c]]; }, 0xffffffffu);
+            double v = vals[L];
+            cs.E[j * kES16 + j2] = v;
+            cs.E[j2 * kES16 + j] = v;
         }
-        double v = vals[L];
-        cs.E[j * kES16 + j2] = v;
-        cs.E[j2 * kES16 + j] = v;
+    } else {  // one warp per pair (warp_bottleneck on a staged key block)
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int MW = min(kMatchWarps, (int)(blockDim.x >> 5)), ks = m | 1;
+        if (wid < MW) {
+            uint32_t* wk = cs.wk + (size_t)wid * m * ks;
+            for (int tt = wid; tt < npairs; tt += MW) {
+                int j, j2;
+                decode_pair(tt, k, j, j2);
+                const int16_t* A = mem + j * m;
+                const int16_t* B = mem + j2 * m;
+                for (int c = lane; c < m; c += kWarp) {
+                    const int bc = B[c];
+                    for (int r = 0; r < m; r++) wk[r * ks + c] = (uint32_t)RK[(size_t)A[r] * rs + bc];
+                }
+                __syncwarp();
+                const uint32_t L = warp_bottleneck<uint32_t>(m, wk, ks, lane);
+                if (lane == 0) {
+                    const double v = vals[L];
+                    cs.E[j * kES16 + j2] = v;
+                    cs.E[j2 * kES16 + j] = v;
+                }
+                __syncwarp();
+            }
+        }
     }
     if (threadIdx.x < k) cs.E[threadIdx.x * kES16 + threadIdx.x] = 0.0;
     __syncthreads();

@@ -98,6 +98,114 @@ __device__ Key bottleneck_threshold(int m, const At& R, Key key_max) {
     return L;
 }
 
+// Warp-cooperative version of the same value for an m x m key block staged
+// in shared memory (m <= 64, row stride ks odd so row-wise and column-wise
+// lane reads are both conflict-free).  Lane l owns columns l and l + 32:
+// their adjacency over rows at the current threshold (u64), the row they
+// are matched to and their BFS parent.  Per inserted row, a BFS level is
+// two ballots (columns newly reached, free ones among them) and two OR
+// reductions (their matched rows join the tree); a Hall violator raises the
+// threshold to the warp-wide minimum key leaving the tree, exactly as
+// bottleneck_threshold does, so the returned key is the same (the
+// bottleneck of a matrix does not depend on which matching attains it).
+template <typename Key>
+__device__ Key warp_bottleneck(int m, const Key* K, int ks, int lane) {
+    constexpr unsigned kF = 0xffffffffu;
+    const int c0 = lane, c1 = lane + 32;
+    const bool h0 = c0 < m, h1 = c1 < m;
+    // lower bound: max of the row minima and the column minima
+    unsigned lb = 0;
+    {
+        Key cm0 = (Key)~(Key)0, cm1 = cm0, rm0 = cm0, rm1 = cm0;
+        for (int i = 0; i < m; i++) {
+            if (h0) {
+                const Key a = K[i * ks + c0], b = K[c0 * ks + i];
+                cm0 = a < cm0 ? a : cm0;
+                rm0 = b < rm0 ? b : rm0;
+            }
+            if (h1) {
+                const Key a = K[i * ks + c1], b = K[c1 * ks + i];
+                cm1 = a < cm1 ? a : cm1;
+                rm1 = b < rm1 ? b : rm1;
+            }
+        }
+        if (h0) lb = max(lb, (unsigned)max(cm0, rm0));
+        if (h1) lb = max(lb, (unsigned)max(cm1, rm1));
+    }
+    Key L = (Key)__reduce_max_sync(kF, lb);
+    uint64_t at0 = 0, at1 = 0;  // rows r with K[r][c] <= L
+    auto build = [&]() {
+        at0 = at1 = 0;
+        for (int r = 0; r < m; r++) {
+            if (h0 && K[r * ks + c0] <= L) at0 |= 1ull << r;
+            if (h1 && K[r * ks + c1] <= L) at1 |= 1ull << r;
+        }
+    };
+    build();
+    int mc0 = -1, mc1 = -1;  // row matched to column c0 / c1
+    int mr0 = -1, mr1 = -1;  // column matched to row lane / lane + 32
+    for (int u = 0; u < m; u++) {
+        uint64_t rows_in = 1ull << u, cols_in = 0, F = rows_in;
+        int p0 = -1, p1 = -1, found = -1;
+        for (;;) {
+            const bool n0 = h0 && !(cols_in >> c0 & 1ull) && (at0 & F);
+            const bool n1 = h1 && !(cols_in >> c1 & 1ull) && (at1 & F);
+            if (n0) p0 = __ffsll((long long)(at0 & F)) - 1;
+            if (n1) p1 = __ffsll((long long)(at1 & F)) - 1;
+            const uint64_t nc = (uint64_t)__ballot_sync(kF, n0) | ((uint64_t)__ballot_sync(kF, n1) << 32);
+            if (nc) {
+                cols_in |= nc;
+                const uint64_t fr = (uint64_t)__ballot_sync(kF, n0 && mc0 < 0) |
+                                    ((uint64_t)__ballot_sync(kF, n1 && mc1 < 0) << 32);
+                if (fr) {
+                    found = __ffsll((long long)fr) - 1;
+                    break;
+                }
+                // every new column is matched: its row joins the tree
+                unsigned lo = 0, hi = 0;
+                if (n0) (mc0 < 32 ? lo : hi) |= 1u << (mc0 & 31);
+                if (n1) (mc1 < 32 ? lo : hi) |= 1u << (mc1 & 31);
+                lo = __reduce_or_sync(kF, lo);
+                hi = __reduce_or_sync(kF, hi);
+                F = ((uint64_t)hi << 32) | lo;
+                rows_in |= F;
+                continue;
+            }
+            // Hall violator: raise to the cheapest edge leaving the tree
+            unsigned x = 0xffffffffu;
+            for (uint64_t rs = rows_in; rs; rs &= rs - 1) {
+                const int r = __ffsll((long long)rs) - 1;
+                if (h0 && !(cols_in >> c0 & 1ull)) x = min(x, (unsigned)K[r * ks + c0]);
+                if (h1 && !(cols_in >> c1 & 1ull)) x = min(x, (unsigned)K[r * ks + c1]);
+            }
+            L = (Key)__reduce_min_sync(kF, x);
+            build();
+            F = rows_in;
+        }
+        // flip the alternating path found -> ... -> u
+        int c = found;
+        for (;;) {
+            const int r = __shfl_sync(kF, c < 32 ? p0 : p1, c & 31);
+            const int pc = __shfl_sync(kF, r < 32 ? mr0 : mr1, r & 31);
+            if (lane == (c & 31)) {
+                if (c < 32)
+                    mc0 = r;
+                else
+                    mc1 = r;
+            }
+            if (lane == (r & 31)) {
+                if (r < 32)
+                    mr0 = c;
+                else
+                    mr1 = c;
+            }
+            if (r == u) break;
+            c = pc;
+        }
+    }
+    return L;
+}
+
 // ---------------------------------------------------------------------------
 // 8 x 8 bottleneck matching, register resident.
 //
