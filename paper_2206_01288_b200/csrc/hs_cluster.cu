@@ -107,16 +107,10 @@ __device__ __forceinline__ double tree_min(const double (&c)[NV]) {
     return x[0];
 }
 
-// HS_HK_ILP=1: two tasks per iteration with min trees (needs ~100 registers,
-// so one CTA per SM); measured slower than two 64-register CTAs per SM
-#ifndef HS_HK_ILP
-#define HS_HK_ILP 0
-#endif
-#if HS_HK_ILP
 // One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
 // w[.][v] for v in r stay in registers while every u not in r is relaxed,
-// two u at a time (independent loads / adds / min trees for ILP; one CTA
-// per SM leaves 128 registers per thread).
+// two u at a time (independent loads / adds / min trees: ILP at the 64
+// registers two CTAs per SM leave).
 template <int NV>
 __device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
                                            uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
@@ -156,51 +150,6 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
     }
 }
 
-#else
-// One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
-// w[.][v] for v in r stay in registers while every u not in r is relaxed,
-// two u at a time (independent loads / adds / min trees for ILP; one CTA
-// per SM leaves 128 registers per thread).
-template <int NV>
-__device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
-                                           uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
-                                           double* const* dst) {
-    uint32_t r = (uint32_t)(rw & 0xFFFF);
-    const int lr = (int)(rw >> 16) & 0x1FFFF;
-    const bool straddle = (rw >> 33) & 1;
-    const uint32_t* dw = dwords + (rw >> 34);
-    double hv[NV];
-    const char* ev[NV];  // &w[0][v]
-#pragma unroll
-    for (int i = 0; i < NV; i++) {
-        const int v = __ffs(r) - 1;
-        r &= r - 1;
-        ev[i] = reinterpret_cast<const char*>(Es) + v * 8;
-        const int li = lr + i;
-        hv[i] = (!straddle || li < Cin) ? own[li] : next[li - Cin];
-    }
-    uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
-    for (int j = 0; rest; j += 2) {
-        const int u0 = __ffs(rest) - 1;
-        rest &= rest - 1;
-        const bool two = rest != 0;
-        const int u1 = two ? __ffs(rest) - 1 : u0;
-        rest &= rest - 1;
-        const uint32_t d0 = __ldg(dw + j);
-        const uint32_t d1 = two ? __ldg(dw + j + 1) : 0u;
-        const int o0 = u0 * kES16 * 8, o1 = u1 * kES16 * 8;
-        double c0[NV], c1[NV];
-#pragma unroll
-        for (int i = 0; i < NV; i++) {
-            c0[i] = *reinterpret_cast<const double*>(ev[i] + o0) + hv[i];
-            c1[i] = *reinterpret_cast<const double*>(ev[i] + o1) + hv[i];
-        }
-        dst[d0 >> 17][d0 & 0x1FFFF] = tree_min<NV>(c0);
-        if (two) dst[d1 >> 17][d1 & 0x1FFFF] = tree_min<NV>(c1);
-    }
-}
-
-#endif
 
 // layer 2: r = {v}, h[r][v] = 0 (implicit): h[{u, v}][u] = w[u][v]
 __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, uint32_t full,
@@ -217,8 +166,12 @@ __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, 
     }
 }
 
-// two 512-thread CTAs per SM (64 registers): 16-CTA clusters cover 8 SMs,
-// 18 co-resident clusters instead of 7 (config 4: 122k -> 141k evals/s)
+// two 512-thread CTAs per SM (64 registers, a few spilled): 16-CTA clusters
+// cover 8 SMs, 18 co-resident clusters instead of 7 (config 4: 122k -> 141k
+// evals/s).  Measured and rejected: the serial min chain at 64 registers
+// (83k), tasks split into parts of 2-8 u (no gain: the stalls are the layer
+// barriers, not the last wave), a per-CTA mbarrier layer barrier instead
+// of barrier.cluster (79k).
 #ifndef HS_HK_MINB
 #define HS_HK_MINB 2
 #endif
