@@ -222,6 +222,8 @@ def run_ours():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
+        print(f"[bench rank {rank}] NCCL_DEBUG={os.environ.get('NCCL_DEBUG')} "
+              f"NCCL_DEBUG_SUBSYS={os.environ.get('NCCL_DEBUG_SUBSYS')}", file=sys.stderr, flush=True)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         dist.barrier()
     dev = torch.device(f"cuda:{local}")
@@ -536,7 +538,22 @@ def sweep_legs(local):
             str(P): rate(g, PAPER_WORKLOAD, P) for P in (1 << 10, 1 << 14, 1 << 18, 1 << 20)}
     g4 = config4_scenario().graph()
     w4 = WorkloadSpec(16, 32, 268_435_456, 201_326_592)
-    out["config4_512dev_16x32_evals_per_s"] = rate(g4, w4, 2048, reps=2)
+    out["config4_512dev_16x32_evals_per_s"] = rate(g4, w4, 16384, reps=2)
+    # config 4's "island model": one GA island per SM (CTA islands, d_pp = 16
+    # pricing inside the GA kernel), a few generations; evaluations counted
+    # from the islands' own results
+    icfg = S.ScheduleConfig(pop_size=16, generations=3, local_search="ours", seed=5)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    sess = S.GASession(g4, w4, icfg, S.island_seeds(icfg.seed, sms))
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    sess.run(icfg.generations)
+    res = sess.results()
+    t_isl = time.perf_counter() - t0
+    out["config4_islands"] = {"islands": sms, "generations": icfg.generations, "pop_size": icfg.pop_size,
+                              "seconds": t_isl, "island_generations_per_s": sms * icfg.generations / t_isl,
+                              "evals_per_s": sum(r.evaluations for r in res) / t_isl,
+                              "what": "one CTA island per SM, 512 devices 16x32, ours, incl. init pricing"}
     g5 = random_graph(0, 1024)
     out["config5_1024dev_16x64_evals_per_s"] = rate(g5, WorkloadSpec(16, 64, 1 << 30, 3 << 26), 1024, reps=2)
     out["config5_1024dev_32x32_heuristic_evals_per_s"] = rate(g5, WorkloadSpec(32, 32, 1 << 30, 3 << 26), 4096,
@@ -568,7 +585,9 @@ def self_launch(n: int) -> int:
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
-    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"),
+               NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"),
+               NCCL_DEBUG_SUBSYS=os.environ.get("NCCL_DEBUG_SUBSYS", "INIT"))
     return subprocess.call(cmd, env=env)
 
 
