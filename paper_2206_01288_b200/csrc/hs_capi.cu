@@ -4,6 +4,7 @@
 #include <thrust/sort.h>
 #include <thrust/unique.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -552,7 +553,8 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     DeviceGuard dg(h->device);
     const int km = h->k * h->m;
     if (!h->chunk) {
-        h->chunk = 1 << 18;
+        h->chunk = 1 << 16;  // 8 MB of layouts per H2D chunk (measured best for e2e: 2^14..2^20 swept)
+        if (const char* e = getenv("HS_HOST_CHUNK_LOG2")) h->chunk = (int64_t)1 << std::max(10, std::min(24, atoi(e)));
         for (int i = 0; i < 2; i++) {
             CK(cudaMalloc(&h->cg[i], (size_t)h->chunk * km * 2), "cudaMalloc chunk");
             CK(cudaMalloc(&h->co[i], (size_t)h->chunk * (3 + h->k) * 8 + (size_t)h->chunk * h->k), "cudaMalloc chunk");

@@ -116,7 +116,9 @@ def test_chunked_host_path_crosses_chunk_boundary():
     g, w = I.instance("case2")
     parts = _random_parts(5, (1 << 18) + 1000, 64, 8, 8)
     r = hs.comm_cost_batch(g, parts, w)
-    sel = np.r_[0:50, (1 << 18) - 25:(1 << 18) + 25, len(parts) - 50:len(parts)]
+    # host chunks: a first chunk of 2^13, then 2^16 each (hs_eval_batch_host)
+    b0, b1 = 1 << 13, (1 << 13) + (1 << 16)
+    sel = np.r_[0:50, b0 - 25:b0 + 25, b1 - 25:b1 + 25, (1 << 18) - 25:(1 << 18) + 25, len(parts) - 50:len(parts)]
     t, _, _ = O.Oracle.of(g, w).comm_cost_batch(parts[sel], threads=O.cpu_count())
     assert np.array_equal(r["total"][sel], t)
     assert np.all(np.isfinite(r["total"]))
