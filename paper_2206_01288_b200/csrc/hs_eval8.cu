@@ -25,6 +25,8 @@
 // takes a free set, writes the edges, runs Held-Karp and hands the set back.
 // That doubles the resident warps (16 per SM at <= 128 registers) that the
 // 227 KB of shared memory allowed with one private set per warp.
+#include <cstdlib>
+
 #include "hs_hk8_gen.cuh"
 #include "hs_match8_dp.cuh"
 #include "hs_tma.cuh"
@@ -66,7 +68,10 @@ __device__ __forceinline__ double shfl_xor_d(double x, int m) {
 
 __device__ __forceinline__ int i16(uint32_t w, int hi) { return hi ? (int)(int16_t)(w >> 16) : (int)(int16_t)(w & 0xFFFFu); }
 
-template <bool kPerGroup>
+// kC = candidates per warp: 4 (throughput: lane (c, g)) or 1 (latency mode
+// for small batches: every 8-lane group mirrors candidate 0's groups, its
+// 28 matchings take one round, only lanes 0..7's Held-Karp result is used).
+template <bool kPerGroup, int kC>
 __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t* offs = reinterpret_cast<uint32_t*>(smem);
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
     for (int i = 0; i < 4; i++) {
         const int t = lane + 32 * i;
         job[i] = 0;
-        if (t < 112) {
+        if (t < 28 * kC) {
             const int cc = t / 28, pi = t - cc * 28;
             int j, j2;
             decode_pair(pi, 8, j, j2);
@@ -140,9 +145,11 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         }
     }
 
-    for (int64_t q = (int64_t)blockIdx.x * W + wid; q * 4 < a.P; q += (int64_t)gridDim.x * W) {
-        const int64_t p = q * 4 + c;
-        const bool live = p < a.P;
+    // latency mode: consecutive candidates on different CTAs (SMs) first
+    const int64_t q0 = kC == 4 ? (int64_t)blockIdx.x * W + wid : (int64_t)wid * gridDim.x + blockIdx.x;
+    for (int64_t q = q0; q * kC < a.P; q += (int64_t)gridDim.x * W) {
+        const int64_t p = q * kC + (kC == 4 ? c : 0);
+        const bool live = (kC == 4 || c == 0) && p < a.P;
         uint4 gm = live ? __ldg(gsrc + p * 8 + g) : ident;
         // validation: in range, ascending, the candidate's 8 groups cover 0..63
         int mem[8];
@@ -280,17 +287,28 @@ bool eval8_applicable(const EvalArgs& a, size_t smem_optin) {
            ((uintptr_t)a.groups & 15) == 0;
 }
 
+template <int kC>
+static void launch_eval8_c(const EvalArgs& a, int blocks, cudaStream_t s) {
+    if (a.per_group) {
+        cudaFuncSetAttribute(eval8_kernel<true, kC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
+        eval8_kernel<true, kC><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(eval8_kernel<false, kC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
+        eval8_kernel<false, kC><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+    }
+}
+
 int launch_eval8(const EvalArgs& a, int sm_count, cudaStream_t s) {
     if (a.P == 0) return 0;
-    const int64_t quads = (a.P + 3) / 4;
-    // small batches: spread the quads over every SM (a quad's latency is the floor)
-    const int blocks = (int)std::min<int64_t>(sm_count, quads);
-    if (a.per_group) {
-        cudaFuncSetAttribute(eval8_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
-        eval8_kernel<true><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+    // small batches: one candidate per warp when the batch does not fill
+    // the GPU's warps (a warp's latency is the floor), else four
+    static const int64_t kLatencyMax = getenv("HS_E8_LATENCY_MAX") ? atoll(getenv("HS_E8_LATENCY_MAX")) : -1;
+    const int64_t lat_max = kLatencyMax >= 0 ? kLatencyMax : (int64_t)sm_count * kE8Warps;
+    if (a.P <= lat_max) {
+        launch_eval8_c<1>(a, (int)std::min<int64_t>(sm_count, a.P), s);
     } else {
-        cudaFuncSetAttribute(eval8_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kE8Smem);
-        eval8_kernel<false><<<blocks, 32 * kE8Warps, kE8Smem, s>>>(a);
+        const int64_t quads = (a.P + 3) / 4;
+        launch_eval8_c<4>(a, (int)std::min<int64_t>(sm_count, quads), s);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }

@@ -62,3 +62,20 @@ def test_brute_force_vs_oracle(name, max_dev):
     t, _, _ = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
     i = int(np.argmin(t))
     assert [list(x) for x in p.groups] == parts[i].tolist() and cb.total == t[i]
+
+
+@pytest.mark.parametrize("name", ["r16_4x4", "r16_2x8"])
+def test_brute_force_n16_optimum_properties(name):
+    """N = 16 (2.6M balanced 4x4 partitions; §8(f) row 2 asks for 12-16):
+    the oracle re-prices the returned optimum to the same bits, and no
+    partition in a 20k random sample (priced by the oracle) is cheaper."""
+    g, w = I.instance(name)
+    p, cb = hs.brute_force_best(g, w, max_devices=16)
+    orc = O.Oracle.of(g, w)
+    t, _, _ = orc.comm_cost_batch(np.asarray([p.groups], dtype=np.int16))
+    assert t[0] == cb.total
+    rng = np.random.default_rng(16)
+    sample = np.sort(rng.permuted(np.tile(np.arange(16, dtype=np.int16), (20_000, 1)), axis=1)
+                     .reshape(-1, w.d_pp, w.d_dp), axis=2)
+    ts, _, _ = orc.comm_cost_batch(sample, threads=O.cpu_count())
+    assert ts.min() >= cb.total
