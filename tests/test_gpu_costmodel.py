@@ -360,3 +360,20 @@ def test_host_path_from_two_threads_on_one_handle():
         got = list(ex.map(lambda p: hs.comm_cost_batch(g, p, w)["total"], pops))
     for r, x in zip(ref, got):
         assert np.array_equal(r, x)
+
+
+@pytest.mark.parametrize("name", ["config4", "config5"])
+def test_config45_extra_reference_vectors(name):
+    """Every reference-priced config-4/5 layout of big_extra.npz, through the
+    stage + cluster path (no order) and the CTA path (order, per-group)."""
+    d = np.load(I.GOLDEN / "big_extra.npz")
+    g, w = I.instance(name)
+    parts = d[f"{name}/parts"]
+    fast = hs.comm_cost_batch(g, parts, w)
+    full = hs.comm_cost_batch(g, parts, w, per_group=True, order=True)
+    for r in (fast, full):
+        assert np.array_equal(r["total"], d[f"{name}/total"])
+        assert np.array_equal(r["datap"], d[f"{name}/datap"])
+        assert np.array_equal(r["pipelinep"], d[f"{name}/pipelinep"])
+    assert np.array_equal(full["per_group"], d[f"{name}/per_group"])
+    assert np.array_equal(full["order"], d[f"{name}/order"])

@@ -229,3 +229,16 @@ def test_oracle_config5_heuristic_and_passes():
         ch, out = orc.one_pass(np.array(c["groups"], dtype=np.int32), c["kind"], st, c["phase"])
         assert ch == c["changed"] and out.tolist() == c["out"]
         assert _rng_after(st) == c["rng_after"]
+
+
+def test_oracle_matches_reference_config45_extra():
+    """tests/golden/big_extra.npz: 32 config-4 and 12 config-5 layouts priced
+    by the reference's comm_cost (make_golden_big.py)."""
+    import numpy as np
+    d = np.load(I.GOLDEN / "big_extra.npz")
+    for name in ("config4", "config5"):
+        g, w = I.instance(name)
+        parts = d[f"{name}/parts"][:6]  # the oracle's k = 16 Held-Karp is the slow part
+        t, dp, pp = O.Oracle.of(g, w).comm_cost_batch(parts, threads=O.cpu_count())
+        assert np.array_equal(t, d[f"{name}/total"][:6]) and np.array_equal(dp, d[f"{name}/datap"][:6])
+        assert np.array_equal(pp, d[f"{name}/pipelinep"][:6])
