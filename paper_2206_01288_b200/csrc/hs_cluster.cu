@@ -23,12 +23,14 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <map>
 #include <mutex>
 #include <vector>
 
 #include "hs_cluster.h"
 #include "hs_cta_eval.cuh"
+#include "hs_tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -107,17 +109,82 @@ __device__ __forceinline__ double tree_min(const double (&c)[NV]) {
     return x[0];
 }
 
-// One source block r (NV = p - 1 members): h[r][.] and the byte offsets of
-// w[.][v] for v in r stay in registers while every u not in r is relaxed,
-// two u at a time (independent loads / adds / min trees: ILP at the 64
-// registers two CTAs per SM leave).
+// ---------------------------------------------------------------------------
+// cluster plumbing: asynchronous DSMEM pushes completing on the owner's
+// mbarrier (st.async ... complete_tx) and a relaxed cluster barrier that only
+// orders layers (no release fence: data visibility comes from the mbarrier)
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t a, uint32_t q) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(q));
+    return r;
+}
+__device__ __forceinline__ void cl_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cl_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+__device__ __forceinline__ void push_f64(uint32_t addr, double v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr), "d"(v),
+                 "r"(mbar)
+                 : "memory");
+}
+// announce a phase's bytes (the one arrival of the phase); pushes may land
+// before it (the tx-count goes transiently negative: scripts/probes/stas_probe)
+__device__ __forceinline__ void expect_bytes(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+// phase wait; traps instead of hanging if a phase never completes (a
+// schedule bug must fail the launch, not wedge the GPU)
+__device__ __forceinline__ void layer_wait(uint32_t mbar, uint32_t parity) {
+    uint32_t done;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+    if (done) return;
+    const long long t0 = clock64();
+    for (;;) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+        if (done) return;
+#ifdef HS_HK_DEBUG
+        if (clock64() - t0 > 4000000000LL) {
+            uint64_t raw;
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(mbar));
+            if ((threadIdx.x & 31) == 0)
+                printf("hk timeout: rank %u tid %d mbar %u parity %u raw %016llx\n", cluster_rank(), threadIdx.x, mbar,
+                       parity, (unsigned long long)raw);
+            return;
+        }
+#else
+        if (clock64() - t0 > 20000000000LL) __trap();
+#endif
+    }
+}
+
+// Where layer p's results go: buffer (p & 1) of the destination CTA, counted
+// on that CTA's mbarrier (p & 1).  delta[q] maps a local shared address to
+// CTA q's copy (offsets within a CTA's window are preserved).
+struct PushTo {
+    uint32_t buf;   // local shared address of the destination buffer
+    uint32_t mbar;  // local shared address of the destination mbarrier
+    const uint32_t* delta;
+    __device__ __forceinline__ void put(uint32_t d, double v) const {
+        const uint32_t dq = delta[d >> 17];
+        push_f64(buf + (d & 0x1FFFFu) * 8u + dq, v, mbar + dq);
+    }
+};
+
+// One source block r (NV = p - 1 members): h[r][.] (own shared memory) and
+// the byte offsets of w[.][v] for v in r stay in registers while every u not
+// in r is relaxed, two u at a time (independent loads / adds / min trees:
+// ILP at the 64 registers two CTAs per SM leave).
 template <int NV>
-__device__ __forceinline__ void two_source(const double* Es, const double* own, const double* next, int Cin,
-                                           uint64_t rw, uint32_t full, const uint32_t* __restrict__ dwords,
-                                           double* const* dst) {
+__device__ __forceinline__ void two_source(const double* Es, const double* own, uint64_t rw, uint32_t full,
+                                           const uint32_t* __restrict__ dwords, const PushTo& to) {
     uint32_t r = (uint32_t)(rw & 0xFFFF);
     const int lr = (int)(rw >> 16) & 0x1FFFF;
-    const bool straddle = (rw >> 33) & 1;
     const uint32_t* dw = dwords + (rw >> 34);
     double hv[NV];
     const char* ev[NV];  // &w[0][v]
@@ -126,8 +193,7 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
         const int v = __ffs(r) - 1;
         r &= r - 1;
         ev[i] = reinterpret_cast<const char*>(Es) + v * 8;
-        const int li = lr + i;
-        hv[i] = (!straddle || li < Cin) ? own[li] : next[li - Cin];
+        hv[i] = own[lr + i];
     }
     uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
     for (int j = 0; rest; j += 2) {
@@ -145,15 +211,14 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
             c0[i] = *reinterpret_cast<const double*>(ev[i] + o0) + hv[i];
             c1[i] = *reinterpret_cast<const double*>(ev[i] + o1) + hv[i];
         }
-        dst[d0 >> 17][d0 & 0x1FFFF] = tree_min<NV>(c0);
-        if (two) dst[d1 >> 17][d1 & 0x1FFFF] = tree_min<NV>(c1);
+        to.put(d0, tree_min<NV>(c0));
+        if (two) to.put(d1, tree_min<NV>(c1));
     }
 }
 
-
 // layer 2: r = {v}, h[r][v] = 0 (implicit): h[{u, v}][u] = w[u][v]
 __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, uint32_t full,
-                                                 const uint32_t* __restrict__ dwords, double* const* dst) {
+                                                 const uint32_t* __restrict__ dwords, const PushTo& to) {
     const uint32_t r = (uint32_t)(rw & 0xFFFF);
     const int v = __ffs(r) - 1;
     const uint32_t* dw = dwords + (rw >> 34);
@@ -161,17 +226,26 @@ __device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, 
     for (int j = 0; rest; j++) {
         const int u = __ffs(rest) - 1;
         rest &= rest - 1;
-        const uint32_t d = __ldg(dw + j);
-        dst[d >> 17][d & 0x1FFFF] = Es[u * kES16 + v];  // w[u][v] + 0.0
+        to.put(__ldg(dw + j), Es[u * kES16 + v]);  // w[u][v] + 0.0
     }
 }
 
-// two 512-thread CTAs per SM (64 registers, a few spilled): 16-CTA clusters
-// cover 8 SMs, 18 co-resident clusters instead of 7 (config 4: 122k -> 141k
-// evals/s).  Measured and rejected: the serial min chain at 64 registers
-// (83k), tasks split into parts of 2-8 u (no gain: the stalls are the layer
-// barriers, not the last wave), a per-CTA mbarrier layer barrier instead
-// of barrier.cluster (79k).
+// Layer sequencing per candidate (k - 1 layers, p = 2..k):
+//   wait    cluster barrier: every CTA finished layer p - 1's tasks, so no
+//           CTA still reads buffer (p & 1) (it held layer p - 2), and every
+//           thread here has seen mbarrier (p & 1)'s previous phase complete;
+//           thread 0 announces layer p's bytes on it (announcing earlier
+//           could complete a 0-byte phase while a slow thread still waits on
+//           the previous one with the same parity: measured, a hang)
+//   wait    own mbarrier (p - 1) & 1: all of layer p - 1 has landed here
+//   tasks   push layer p
+//   arrive  (relaxed)
+// After layer k, the full set's entries are read on CTA 0 before the last
+// arrive.  Two 512-thread CTAs per SM (64
+// registers): 16-CTA clusters cover 8 SMs, 18 co-resident clusters.
+// Measured and rejected (round 2): the serial min chain at 64 registers,
+// tasks split into parts of 2-8 u, a per-CTA mbarrier layer barrier with
+// plain DSMEM stores and release fences.
 #ifndef HS_HK_MINB
 #define HS_HK_MINB 2
 #endif
@@ -182,66 +256,82 @@ __global__ void __launch_bounds__(kClusterThreads, HS_HK_MINB) hk_cluster_kernel
                                                                      double* __restrict__ out_total,
                                                                      double* __restrict__ out_pipe) {
     extern __shared__ __align__(16) double sm2[];
-    cg::cluster_group cl = cg::this_cluster();
-    const int rank = (int)cl.block_rank(), cs = t.cs;
-    double* buf[2] = {sm2, sm2 + t.Cmax};
+    __shared__ __align__(8) uint64_t mb[2];
+    __shared__ uint32_t delta[16];
+    const int rank = (int)cluster_rank(), cs = t.cs;
     double* Es = sm2 + 2 * t.Cmax;
-    __shared__ double* rb[2][16];
-    if (threadIdx.x < cs) {
-        rb[0][threadIdx.x] = cl.map_shared_rank(buf[0], (int)threadIdx.x);
-        rb[1][threadIdx.x] = cl.map_shared_rank(buf[1], (int)threadIdx.x);
+    const uint32_t lbuf0 = smem_addr(sm2), lbstride = (uint32_t)t.Cmax * 8u;
+    const uint32_t lmb0 = smem_addr(&mb[0]);  // mb[1] is 8 bytes further
+    const int64_t ncl = gridDim.x / cs;
+    if (threadIdx.x < cs) delta[threadIdx.x] = mapa_rank(lbuf0, threadIdx.x) - lbuf0;
+    if (threadIdx.x == 0) {
+        mbar_init(&mb[0], 1);
+        mbar_init(&mb[1], 1);
     }
     __syncthreads();
-    const int64_t ncl = gridDim.x / cs;
+    cg::this_cluster().sync();  // mbarrier inits visible cluster-wide
+    cl_arrive_relaxed();
+    uint32_t phase = 0;  // bit b: parity of the next phase of mb[b]
+    const uint32_t full = (1u << k) - 1u;
     for (int64_t b = blockIdx.x / cs; b < B; b += ncl) {
-        const bool skip = bad && bad[b];  // same for every CTA of the cluster
-        if (!skip) {
-            const double* src = E + b * estride;
-            for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
-                const int rr = i / k, cc = i - rr * k;
-                Es[rr * kES16 + cc] = src[(size_t)rr * es + cc];
+        if (bad && bad[b]) {  // the same for every CTA of the cluster: no layer, no barrier
+            if (rank == 0 && threadIdx.x == 0) {
+                const double nan = __longlong_as_double(0x7ff8000000000000LL);
+                out_total[b] = nan;
+                if (out_pipe) out_pipe[b] = nan;
             }
+            continue;
         }
-        HS_JITTER();
+        __syncthreads();  // every task of the previous candidate read Es
+        const double* src = E + b * estride;
+        for (int i = threadIdx.x; i < k * k; i += blockDim.x) {
+            const int rr = i / k, cc = i - rr * k;
+            Es[rr * kES16 + cc] = src[(size_t)rr * es + cc];
+        }
         __syncthreads();
-        cl.sync();  // every reader of the previous candidate is done
-        if (!skip) {
-            const uint32_t full = (1u << k) - 1u;
-            for (int p = 2; p <= k; p++) {
-                const double* own = buf[(p - 1) & 1];
-                const double* next = rank + 1 < cs ? rb[(p - 1) & 1][rank + 1] : own;
-                double* const* dst = rb[p & 1];
-                const int Cin = t.C[p - 1];
-                const int end = t.rbeg[p][rank + 1];
-                HS_JITTER();
-                for (int x = t.rbeg[p][rank] + (int)threadIdx.x; x < end; x += blockDim.x) {
-                    const uint64_t rw = __ldg(t.rwords + x);
-                    switch (p) {
-                        case 2: two_source_first(Es, rw, full, t.dwords, dst); break;
-                        case 3: two_source<2>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 4: two_source<3>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 5: two_source<4>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 6: two_source<5>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 7: two_source<6>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 8: two_source<7>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 9: two_source<8>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 10: two_source<9>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 11: two_source<10>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 12: two_source<11>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 13: two_source<12>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 14: two_source<13>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        case 15: two_source<14>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                        default: two_source<15>(Es, own, next, Cin, rw, full, t.dwords, dst); break;
-                    }
-                }
-                HS_JITTER();
-                cl.sync();
+        for (int p = 2; p <= k; p++) {
+            HS_JITTER();
+            cl_wait();
+            if (threadIdx.x == 0)
+                expect_bytes(lmb0 + 8 * (p & 1), (uint32_t)((t.sbeg[p][rank + 1] - t.sbeg[p][rank]) * p * 8));
+            if (p >= 3) {
+                const int pb = (p - 1) & 1;
+                layer_wait(lmb0 + 8 * pb, (phase >> pb) & 1u);
+                phase ^= 1u << pb;
             }
-            if (rank == 0 && threadIdx.x == 0) {  // layer k: the full set's k entries, slots 0..k-1
-                const int Ck = t.C[k];
-                double* const* fin = rb[k & 1];
-                double tot = fin[0][0];
-                for (int u = 1; u < k; u++) tot = dmin(tot, fin[u / Ck][u % Ck]);
+            const PushTo to{lbuf0 + (p & 1) * lbstride, lmb0 + 8 * (p & 1), delta};
+            const double* own = sm2 + ((p - 1) & 1) * t.Cmax;
+            const int end = t.rbeg[p][rank + 1];
+            for (int x = t.rbeg[p][rank] + (int)threadIdx.x; x < end; x += blockDim.x) {
+                const uint64_t rw = __ldg(t.rwords + x);
+                switch (p) {
+                    case 2: two_source_first(Es, rw, full, t.dwords, to); break;
+                    case 3: two_source<2>(Es, own, rw, full, t.dwords, to); break;
+                    case 4: two_source<3>(Es, own, rw, full, t.dwords, to); break;
+                    case 5: two_source<4>(Es, own, rw, full, t.dwords, to); break;
+                    case 6: two_source<5>(Es, own, rw, full, t.dwords, to); break;
+                    case 7: two_source<6>(Es, own, rw, full, t.dwords, to); break;
+                    case 8: two_source<7>(Es, own, rw, full, t.dwords, to); break;
+                    case 9: two_source<8>(Es, own, rw, full, t.dwords, to); break;
+                    case 10: two_source<9>(Es, own, rw, full, t.dwords, to); break;
+                    case 11: two_source<10>(Es, own, rw, full, t.dwords, to); break;
+                    case 12: two_source<11>(Es, own, rw, full, t.dwords, to); break;
+                    case 13: two_source<12>(Es, own, rw, full, t.dwords, to); break;
+                    case 14: two_source<13>(Es, own, rw, full, t.dwords, to); break;
+                    case 15: two_source<14>(Es, own, rw, full, t.dwords, to); break;
+                    default: two_source<15>(Es, own, rw, full, t.dwords, to); break;
+                }
+            }
+            if (p < k) cl_arrive_relaxed();
+        }
+        {  // layer k: the full set's k entries, slots 0..k-1 of CTA 0
+            const int kb = k & 1;
+            layer_wait(lmb0 + 8 * kb, (phase >> kb) & 1u);
+            phase ^= 1u << kb;
+            if (rank == 0 && threadIdx.x == 0) {
+                const double* fin = sm2 + kb * t.Cmax;
+                double tot = fin[0];
+                for (int u = 1; u < k; u++) tot = dmin(tot, fin[u]);
                 if (add) {
                     out_total[b] = add[b] + tot;
                     if (out_pipe) out_pipe[b] = tot;
@@ -249,13 +339,10 @@ __global__ void __launch_bounds__(kClusterThreads, HS_HK_MINB) hk_cluster_kernel
                     out_total[b] = tot;
                 }
             }
-        } else if (rank == 0 && threadIdx.x == 0) {
-            const double nan = __longlong_as_double(0x7ff8000000000000LL);
-            out_total[b] = nan;
-            if (out_pipe) out_pipe[b] = nan;
         }
+        cl_arrive_relaxed();
     }
-    cl.sync();  // no CTA leaves while a peer may still touch its shared memory
+    cl_wait();  // no CTA leaves while a peer may still push into its shared memory
 }
 
 // ---------------------------------------------------------------------------
@@ -288,10 +375,11 @@ int get_hk_two(int device, int k, HKTwo* out) {
     if (it == g_two.end()) {
         int optin = 0;
         if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) return -1;
-        uint64_t size[18] = {0};
-        for (int p = 1; p <= k; p++) size[p] = binom(k, p) * (uint64_t)p;
-        uint64_t maxS = 0;
-        for (int p = 2; p <= k; p++) maxS = std::max<uint64_t>(maxS, size[p]);
+        auto slice = [&](int cs) {  // longest per-CTA slice, whole sets
+            uint64_t m = 0;
+            for (int p = 2; p <= k; p++) m = std::max<uint64_t>(m, (binom(k, p) + cs - 1) / cs * (uint64_t)p);
+            return m;
+        };
         DeviceHKTwo d;
         d.t.cs = 0;
         // smallest cluster whose CTAs fit two per SM (32 resident warps);
@@ -299,18 +387,31 @@ int get_hk_two(int device, int k, HKTwo* out) {
         for (int pass = 0; pass < 2 && !d.t.cs; pass++) {
             const uint64_t budget = pass == 0 ? (uint64_t)optin / 2 - 2048 : (uint64_t)optin - 1024;
             for (int cs = 1; cs <= 16; cs *= 2) {
-                const uint64_t C = (maxS + cs - 1) / cs;
-                if ((2 * C + 16 * kES16) * 8 <= budget) {
+                if ((2 * slice(cs) + 16 * kES16) * 8 <= budget) {
                     d.t.cs = cs;
                     break;
                 }
             }
         }
         const int cs = d.t.cs;
+        // whole sets per CTA, ceil split (layer k's single set lives on CTA 0)
+        std::vector<std::vector<int>> owner(k + 1);
         d.t.Cmax = 0;
         for (int p = 0; p < 18; p++) {
-            d.t.C[p] = p >= 1 && p <= k ? (int)((size[p] + cs - 1) / cs) : 1;
-            if (p >= 2 && p <= k) d.t.Cmax = std::max(d.t.Cmax, d.t.C[p]);
+            for (int q = 0; q < 17; q++) d.t.sbeg[p][q] = 0;
+            d.t.C[p] = 1;
+            if (p < 1 || p > k) continue;
+            const uint64_t n = binom(k, p);
+            for (int q = 0; q <= cs; q++) d.t.sbeg[p][q] = (int)((n * (uint64_t)q + cs - 1) / (uint64_t)cs);
+            for (int q = cs + 1; q < 17; q++) d.t.sbeg[p][q] = (int)n;
+            int most = 0;
+            owner[p].resize(n);
+            for (int q = 0; q < cs; q++) {
+                most = std::max(most, d.t.sbeg[p][q + 1] - d.t.sbeg[p][q]);
+                for (int i = d.t.sbeg[p][q]; i < d.t.sbeg[p][q + 1]; i++) owner[p][i] = q;
+            }
+            d.t.C[p] = most * p;
+            if (p >= 2) d.t.Cmax = std::max(d.t.Cmax, d.t.C[p]);
         }
         std::vector<int> rank_of((size_t)1 << k, 0), cnt(k + 2, 0);
         for (int s = 0; s < (1 << k); s++) rank_of[s] = cnt[__builtin_popcount(s)]++;
@@ -326,27 +427,27 @@ int get_hk_two(int device, int k, HKTwo* out) {
                 per[q].clear();
                 perd[q].clear();
             }
-            const uint64_t Cin = (uint64_t)d.t.C[p - 1], Cout = (uint64_t)d.t.C[p];
             int spread = 0;
-            for (int r = 1; r < (1 << k); r++) {  // sources in slot order of layer p-1
+            for (int r = 1; r < (1 << k); r++) {  // sources in rank order of layer p-1
                 if (__builtin_popcount(r) != p - 1) continue;
                 uint64_t w = (uint64_t)r;
-                int owner;
+                int o;
                 if (p >= 3) {
-                    const uint64_t slot = (uint64_t)rank_of[r] * (uint64_t)(p - 1);
-                    owner = (int)(slot / Cin);
-                    const uint64_t lr = slot % Cin;
-                    w |= (lr << 16) | ((lr + (uint64_t)(p - 1) > Cin) ? (1ull << 33) : 0ull);
+                    o = owner[p - 1][rank_of[r]];
+                    const uint64_t lr = (uint64_t)(rank_of[r] - d.t.sbeg[p - 1][o]) * (uint64_t)(p - 1);
+                    w |= lr << 16;
                 } else {
-                    owner = spread++ % cs;  // layer 1 is implicit zeros: deal sources round-robin
+                    o = spread++ % cs;  // layer 1 is implicit zeros: deal sources round-robin
                 }
-                w |= (uint64_t)perd[owner].size() << 34;  // relative; rebased below
-                per[owner].push_back(w);
+                w |= (uint64_t)perd[o].size() << 34;  // relative; rebased below
+                per[o].push_back(w);
                 for (int u = 0; u < k; u++) {
                     if (r >> u & 1) continue;
                     const int s = r | (1 << u);
-                    const uint64_t ds = (uint64_t)rank_of[s] * (uint64_t)p + __builtin_popcount(s & ((1 << u) - 1));
-                    perd[owner].push_back((uint32_t)(((ds / Cout) << 17) | (ds % Cout)));
+                    const int q = owner[p][rank_of[s]];
+                    const uint64_t ls = (uint64_t)(rank_of[s] - d.t.sbeg[p][q]) * (uint64_t)p +
+                                        __builtin_popcount(s & ((1 << u) - 1));
+                    perd[o].push_back((uint32_t)(((uint64_t)q << 17) | ls));
                 }
             }
             for (int q = 0; q < cs; q++) {

@@ -12,15 +12,15 @@ constexpr int kStageES = 17;                  // padded stage-graph row (= kES16
 constexpr int kStageStride = 16 * kStageES;   // doubles per staged candidate
 
 // Two-layer Held-Karp schedule, "push" form.  Layer p holds the entries
-// h[s][u], |s| = p, u in s, at slot rank_p(s) * p + (rank of u in s), where
-// rank_p orders the p-subsets as integers; the slots are split into cs
-// balanced slices of C[p] = ceil(size_p / cs), slice q living in the shared
-// memory of CTA q of the cluster.  Layer p is produced r-major: the CTA that
-// holds h[r][.] (|r| = p - 1) loads those p - 1 values once and computes
-// h[r | u][u] = min_v (w[u][v] + h[r][v]) for every u not in r, storing each
-// result into the slice that owns slot (r | u, u) (a DSMEM store).
+// h[s][u], |s| = p, u in s, at slot (rank_p(s) - sbeg[p][q]) * p + (rank of u
+// in s) of CTA q, where rank_p orders the p-subsets as integers and CTA q owns
+// the sets sbeg[p][q] .. sbeg[p][q + 1] (a balanced split by whole sets, so a
+// set's entries never straddle two CTAs).  Layer p is produced r-major: the
+// CTA that owns r (|r| = p - 1) loads h[r][.] from its own shared memory once
+// and computes h[r | u][u] = min_v (w[u][v] + h[r][v]) for every u not in r,
+// pushing each result into the owner of r | u with an asynchronous DSMEM
+// store that completes on the owner's mbarrier for layer p.
 //   rwords[i]: r (16) | local slot of h[r][first member] (17) << 16 |
-//              "h[r][.] runs into the next CTA's slice" (1) << 33 |
 //              index of r's first destination word (30) << 34
 //   dwords[j]: destination CTA (4) << 17 | local slot (17), one per u not in
 //              r, ascending u
@@ -29,7 +29,8 @@ struct HKTwo {
     const uint64_t* rwords;
     const uint32_t* dwords;
     int rbeg[18][17];
-    int C[18];    // slice length per layer
+    int sbeg[18][17];  // owned p-subsets per CTA (prefix counts)
+    int C[18];    // slice length per layer (entries, max over the CTAs)
     int Cmax;     // buffer length (max over layers)
     int cs;       // CTAs per cluster (1, 2, 4, 8 or 16)
 };
