@@ -176,16 +176,37 @@ struct PushTo {
     }
 };
 
-// One source block r (NV = p - 1 members): h[r][.] (own shared memory) and
-// the byte offsets of w[.][v] for v in r stay in registers while every u not
-// in r is relaxed, two u at a time (independent loads / adds / min trees:
-// ILP at the 64 registers two CTAs per SM leave).
+// Work item (rwords[i]): source set r, local slot of h[r][first member],
+// first destination word, and the item's share of the u not in r (skip the
+// j0 lowest, take cnt).  Layers with few sources split each source's u over
+// several items (one L2 round trip per thread instead of a chain of them).
+struct Item {
+    uint32_t r, rest;
+    int lr, cnt;
+    const uint32_t* dw;
+    __device__ __forceinline__ Item(uint64_t w, uint32_t full, const uint32_t* __restrict__ dwords) {
+        r = (uint32_t)(w & 0xFFFF);
+        lr = (int)(w >> 16) & 0x7FFF;
+        dw = dwords + ((w >> 31) & 0x1FFFFF);
+        const int j0 = (int)(w >> 52) & 0xF;
+        cnt = (int)(w >> 56) & 0x1F;
+        rest = full & ~r;
+        for (int j = 0; j < j0; j++) rest &= rest - 1;
+    }
+};
+
+// One item of source block r (NV = p - 1 members): h[r][.] (own shared
+// memory) and the byte offsets of w[.][v] for v in r stay in registers while
+// the item's u are relaxed, two at a time (independent loads / adds / min
+// trees).  (Loading the destination words one pair ahead costs registers at
+// the 64-register cap: config 4 151k -> 145k, measured.)
 template <int NV>
-__device__ __forceinline__ void two_source(const double* Es, const double* own, uint64_t rw, uint32_t full,
+__device__ __forceinline__ void two_source(const double* Es, const double* own, uint64_t w, uint32_t full,
                                            const uint32_t* __restrict__ dwords, const PushTo& to) {
-    uint32_t r = (uint32_t)(rw & 0xFFFF);
-    const int lr = (int)(rw >> 16) & 0x1FFFF;
-    const uint32_t* dw = dwords + (rw >> 34);
+    Item it(w, full, dwords);
+    uint32_t r = it.r, rest = it.rest;
+    const int cnt = it.cnt;
+    const uint32_t* dw = it.dw;
     double hv[NV];
     const char* ev[NV];  // &w[0][v]
 #pragma unroll
@@ -193,17 +214,15 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
         const int v = __ffs(r) - 1;
         r &= r - 1;
         ev[i] = reinterpret_cast<const char*>(Es) + v * 8;
-        hv[i] = own[lr + i];
+        hv[i] = own[it.lr + i];
     }
-    uint32_t rest = full & ~(uint32_t)(rw & 0xFFFF);
-    for (int j = 0; rest; j += 2) {
+    for (int j = 0; j < cnt; j += 2) {
+        const uint32_t d0 = __ldg(dw + j), d1 = j + 1 < cnt ? __ldg(dw + j + 1) : 0u;
         const int u0 = __ffs(rest) - 1;
         rest &= rest - 1;
-        const bool two = rest != 0;
+        const bool two = j + 1 < cnt;
         const int u1 = two ? __ffs(rest) - 1 : u0;
         rest &= rest - 1;
-        const uint32_t d0 = __ldg(dw + j);
-        const uint32_t d1 = two ? __ldg(dw + j + 1) : 0u;
         const int o0 = u0 * kES16 * 8, o1 = u1 * kES16 * 8;
         double c0[NV], c1[NV];
 #pragma unroll
@@ -217,16 +236,15 @@ __device__ __forceinline__ void two_source(const double* Es, const double* own, 
 }
 
 // layer 2: r = {v}, h[r][v] = 0 (implicit): h[{u, v}][u] = w[u][v]
-__device__ __forceinline__ void two_source_first(const double* Es, uint64_t rw, uint32_t full,
+__device__ __forceinline__ void two_source_first(const double* Es, uint64_t w, uint32_t full,
                                                  const uint32_t* __restrict__ dwords, const PushTo& to) {
-    const uint32_t r = (uint32_t)(rw & 0xFFFF);
-    const int v = __ffs(r) - 1;
-    const uint32_t* dw = dwords + (rw >> 34);
-    uint32_t rest = full & ~r;
-    for (int j = 0; rest; j++) {
+    Item it(w, full, dwords);
+    const int v = __ffs(it.r) - 1;
+    uint32_t rest = it.rest;
+    for (int j = 0; j < it.cnt; j++) {
         const int u = __ffs(rest) - 1;
         rest &= rest - 1;
-        to.put(__ldg(dw + j), Es[u * kES16 + v]);  // w[u][v] + 0.0
+        to.put(__ldg(it.dw + j), Es[u * kES16 + v]);  // w[u][v] + 0.0
     }
 }
 
@@ -427,20 +445,23 @@ int get_hk_two(int device, int k, HKTwo* out) {
                 per[q].clear();
                 perd[q].clear();
             }
+            // u per source, and how many items each source is split into so
+            // that a CTA's items about fill its threads
+            const int U = k - (p - 1);
+            const int tmax = (int)((binom(k, p - 1) + cs - 1) / cs);
+            const int parts = std::max(1, std::min(U, kClusterThreads / std::max(1, tmax)));
             int spread = 0;
             for (int r = 1; r < (1 << k); r++) {  // sources in rank order of layer p-1
                 if (__builtin_popcount(r) != p - 1) continue;
-                uint64_t w = (uint64_t)r;
+                uint64_t lr = 0;
                 int o;
                 if (p >= 3) {
                     o = owner[p - 1][rank_of[r]];
-                    const uint64_t lr = (uint64_t)(rank_of[r] - d.t.sbeg[p - 1][o]) * (uint64_t)(p - 1);
-                    w |= lr << 16;
+                    lr = (uint64_t)(rank_of[r] - d.t.sbeg[p - 1][o]) * (uint64_t)(p - 1);
                 } else {
                     o = spread++ % cs;  // layer 1 is implicit zeros: deal sources round-robin
                 }
-                w |= (uint64_t)perd[o].size() << 34;  // relative; rebased below
-                per[o].push_back(w);
+                const uint64_t dw0 = perd[o].size();  // relative; rebased below
                 for (int u = 0; u < k; u++) {
                     if (r >> u & 1) continue;
                     const int s = r | (1 << u);
@@ -449,15 +470,22 @@ int get_hk_two(int device, int k, HKTwo* out) {
                                         __builtin_popcount(s & ((1 << u) - 1));
                     perd[o].push_back((uint32_t)(((uint64_t)q << 17) | ls));
                 }
+                for (int c = 0, j0 = 0; c < parts; c++) {
+                    const int cnt = U / parts + (c < U % parts ? 1 : 0);
+                    per[o].push_back((uint64_t)r | lr << 16 | (dw0 + j0) << 31 | (uint64_t)j0 << 52 |
+                                     (uint64_t)cnt << 56);
+                    j0 += cnt;
+                }
             }
             for (int q = 0; q < cs; q++) {
                 d.t.rbeg[p][q] = (int)rws.size();
                 const uint64_t base = dws.size();
-                for (uint64_t w : per[q]) rws.push_back(w + (base << 34));
+                for (uint64_t w : per[q]) rws.push_back(w + (base << 31));
                 dws.insert(dws.end(), perd[q].begin(), perd[q].end());
             }
             for (int q = cs; q < 17; q++) d.t.rbeg[p][q] = (int)rws.size();
         }
+        if (d.t.Cmax >= (1 << 15) || dws.size() >= ((size_t)1 << 21)) return -3;  // item word fields
         if (cudaMalloc(&d.rw, rws.size() * 8) != cudaSuccess) return -1;
         if (cudaMalloc(&d.dw, dws.size() * 4) != cudaSuccess) return -1;
         if (cudaMemcpy(d.rw, rws.data(), rws.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return -1;

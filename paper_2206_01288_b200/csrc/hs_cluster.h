@@ -20,11 +20,14 @@ constexpr int kStageStride = 16 * kStageES;   // doubles per staged candidate
 // and computes h[r | u][u] = min_v (w[u][v] + h[r][v]) for every u not in r,
 // pushing each result into the owner of r | u with an asynchronous DSMEM
 // store that completes on the owner's mbarrier for layer p.
-//   rwords[i]: r (16) | local slot of h[r][first member] (17) << 16 |
-//              index of r's first destination word (30) << 34
+//   rwords[i]: one work item: r (16) | local slot of h[r][first member] (15)
+//              << 16 | index of the item's first destination word (21) << 31
+//              | j0 (4) << 52 | cnt (5) << 56 -- the item relaxes the u not
+//              in r after skipping the j0 lowest, cnt of them (layers with
+//              few sources split a source's u over several items)
 //   dwords[j]: destination CTA (4) << 17 | local slot (17), one per u not in
 //              r, ascending u
-// The sources of layer p on CTA q are rwords[rbeg[p][q] .. rbeg[p][q + 1]).
+// The items of layer p on CTA q are rwords[rbeg[p][q] .. rbeg[p][q + 1]).
 struct HKTwo {
     const uint64_t* rwords;
     const uint32_t* dwords;
