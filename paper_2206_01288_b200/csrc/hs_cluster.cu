@@ -261,9 +261,11 @@ __device__ __forceinline__ void two_source_first(const double* Es, uint64_t w, u
 // After layer k, the full set's entries are read on CTA 0 before the last
 // arrive.  Two 512-thread CTAs per SM (64
 // registers): 16-CTA clusters cover 8 SMs, 18 co-resident clusters.
-// Measured and rejected (round 2): the serial min chain at 64 registers,
-// tasks split into parts of 2-8 u, a per-CTA mbarrier layer barrier with
-// plain DSMEM stores and release fences.
+// Measured and rejected (round 2): the serial min chain at 64 registers, a
+// per-CTA mbarrier layer barrier with plain DSMEM stores and release fences,
+// three rotating buffers with the cluster barrier a layer off the critical
+// path (needs one 1,024-thread CTA per SM: config 4 153k -> 127k, the second
+// co-resident cluster per SM is worth more than the barrier slack).
 #ifndef HS_HK_MINB
 #define HS_HK_MINB 2
 #endif
