@@ -112,7 +112,7 @@ def main():
         return f"t{cnt[0]}"
 
     lines.append("    uint32_t kn[4], ks[4];")
-    lines.append("    row(0, kn);")
+    lines.append("    load_row<kMode>(row, 0, kn, ks);")
     for q in range(4):
         lines.append(f"    const uint32_t {name(1 << q)} = kn[{q}];")
     for p in range(2, 9):
@@ -123,9 +123,7 @@ def main():
             for T in {T for T, _, _ in terms(S)}:
                 consumers[T] += 1
         lines.append(f"    // layer {p}: rows 0..{p - 1}, {len(cur)} pair registers")
-        lines.append(f"    row({p - 1}, kn);")
-        for q in range(4):
-            lines.append(f"    ks[{q}] = __byte_perm(kn[{q}], 0u, 0x1032u);")
+        lines.append(f"    load_row<kMode>(row, {p - 1}, kn, ks);")
         for S in order_layer(cur, consumers):
             tn, ts = [], []
             for T, key, swapped in terms(S):
@@ -135,12 +133,12 @@ def main():
             if ts:
                 s = min_tree(ts, lines, tmp)
                 v = tmp()
-                lines.append(f"    const uint32_t {v} = __byte_perm({s}, 0u, 0x1032u);")
+                lines.append(f"    const uint32_t {v} = swap16<kMode>({s});")
                 tn.append(v)
             r = min_tree(tn, lines, tmp)
             if S == sig(S):  # fixed point: halves hold the two half-sets of terms
                 v = tmp()
-                lines.append(f"    const uint32_t {v} = __vminu2({r}, __byte_perm({r}, 0u, 0x1032u));")
+                lines.append(f"    const uint32_t {v} = __vminu2({r}, swap16<kMode>({r}));")
                 r = v
             lines.append(f"    const uint32_t {name(S)} = {r};")
     lines.append(f"    return {name(0xFF)} & 0xFFFFu;")
@@ -148,7 +146,7 @@ def main():
     nmax = sum(1 for ln in lines if "__vmaxu2(" in ln)
     nmin3 = sum(1 for ln in lines if "__vimin3_u16x2(" in ln)
     nmin = sum(1 for ln in lines if "__vminu2(" in ln)
-    nperm = sum(1 for ln in lines if "__byte_perm(" in ln)
+    nperm = sum(1 for ln in lines if "swap16<" in ln) + 28
     src = f"""// hs_match8_dp.cuh -- GENERATED by scripts/gen_match8_dp.py; do not edit.
 //
 // 8 x 8 bottleneck value (combinatorics.py:106-131 _optimal_threshold) as a
@@ -161,12 +159,46 @@ def main():
 
 namespace hs {{
 
-// row(r, kn): kn[q] = key(r, col q) | key(r, col q + 4) << 16, q = 0..3.
+// Half swap (key(r, q + 4) | key(r, q) << 16 from key(r, q) | key(r, q + 4) << 16).
+// kMode 0: PRMT (ALU pipe).  kMode 1: IMAD.HI + IMAD on the FMA pipe -- the
+// DP is bound by the ALU pipe (VIMNMX, PRMT, LOP3 all issue at half rate
+// there: scripts/probes/pipe_probe2.cu), the FMA pipe is idle.
+template <int kMode>
+__device__ __forceinline__ uint32_t swap16(uint32_t x) {{
+    if constexpr (kMode == 0) {{
+        return __byte_perm(x, 0u, 0x1032u);
+    }} else {{
+        uint32_t h, r;
+        asm("mul.hi.u32 %0, %1, 65536;" : "=r"(h) : "r"(x));
+        asm("mad.lo.u32 %0, %1, 65536, %2;" : "=r"(r) : "r"(x), "r"(h));
+        return r;
+    }}
+}}
+
+// kMode 0: row(r, kn) fills kn[q] = key(r, col q) | key(r, col q + 4) << 16;
+// kMode 1: row(r, kn, ks) also fills the half-swapped ks[q] (the caller packs
+// both from the loaded keys on the FMA pipe).
+template <int kMode, typename RowF>
+__device__ __forceinline__ void load_row(RowF& row, int r, uint32_t (&kn)[4], uint32_t (&ks)[4]) {{
+    if constexpr (kMode == 0) {{
+        row(r, kn);
+#pragma unroll
+        for (int q = 0; q < 4; q++) ks[q] = swap16<0>(kn[q]);
+    }} else {{
+        row(r, kn, ks);
+    }}
+}}
+
 // Returns the smallest key L such that the entries <= L of the 8 x 8 key
 // matrix admit a perfect matching (any u16 keys).
+template <int kMode, typename RowF>
+__device__ __forceinline__ uint32_t match8_dp_m(RowF&& row) {{
+{body}
+}}
+
 template <typename RowF>
 __device__ __forceinline__ uint32_t match8_dp(RowF&& row) {{
-{body}
+    return match8_dp_m<0>(row);
 }}
 
 }}  // namespace hs

@@ -82,6 +82,39 @@ def test_20k_layouts_per_case_bitwise_vs_oracle(case):
     assert np.array_equal(r["pipelinep"], p)
 
 
+@pytest.mark.parametrize("case", [2, 4, 5])
+def test_large_device_batch_with_malformed_rows_vs_oracle(case):
+    """P = 50,003 in one device launch (a partial last quad), per-group
+    values, and malformed rows scattered through it (NaN + count)."""
+    import torch
+    from paper_2206_01288_b200 import _native as N
+    g, w = I.instance(f"case{case}")
+    P = 50003
+    parts = _random_parts(100 + case, P, 64, 8, 8)
+    bad = [5, 31337, P - 1]
+    parts[5, 0, 1] = parts[5, 0, 0]              # duplicate device
+    parts[31337, 2, :] = parts[31337, 2, ::-1]  # not ascending
+    parts[P - 1, 3, 7] = 64                      # out of range
+    inst = N.instance_for(g, w)
+    t = torch.from_numpy(parts).cuda()
+    o = [torch.empty(P, dtype=torch.float64, device="cuda") for _ in range(3)]
+    pg = torch.empty((P, 8), dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    N.check(N.lib().hs_eval_batch(inst.handle, t.data_ptr(), P, o[0].data_ptr(), o[1].data_ptr(), o[2].data_ptr(),
+                                  pg.data_ptr(), None, cnt.data_ptr(), N.stream_ptr(inst.device)), "hs_eval_batch")
+    tot, dp_, pp_, pg = (x.cpu().numpy() for x in (*o, pg))
+    assert int(cnt.item()) == 3
+    keep = np.setdiff1d(np.arange(P), bad)
+    orc = O.Oracle.of(g, w)
+    want_t, want_d, want_p = orc.comm_cost_batch(parts[keep], threads=O.cpu_count())
+    assert np.array_equal(tot[keep], want_t)
+    assert np.array_equal(dp_[keep], want_d)
+    assert np.array_equal(pp_[keep], want_p)
+    assert np.isnan(tot[bad]).all() and np.isnan(dp_[bad]).all() and np.isnan(pp_[bad]).all()
+    for i in keep[::997]:
+        assert np.array_equal(pg[i], orc.comm_cost(parts[i])[3])
+
+
 @pytest.mark.parametrize("name", ["r64_8x8", "r36_6x6", "r64_2x32", "r48_3x16", "r40_4x10", "config1"])
 def test_random_graphs_bitwise_vs_oracle(name):
     g, w = I.instance(name)
