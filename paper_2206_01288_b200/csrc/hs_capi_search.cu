@@ -68,6 +68,15 @@ struct hs_ga {
     cudaStream_t last = nullptr;  // stream of the latest run / export / import (hs_ga_result syncs it)
     int spec = -1;                // speculative pipeline cluster size (0: off, -1: not probed yet)
     bool started = false;         // the population has been initialised by a launch
+    // batch-priced generations (d_pp 9..16 on the cluster Held-Karp path):
+    // every island's snapshots of a generation are priced in one batch
+    bool batch = false;
+    int snap_stride = 0;
+    int host_gen = 0;             // generations run so far (islands advance in lockstep)
+    int16_t* snap_buf = nullptr;
+    double* snap_cost = nullptr;
+    int* snap_cnt = nullptr;
+    int32_t* invalid = nullptr;   // the batch pricer's count (padding slots count as malformed)
 };
 
 static hs::GAArgs ga_args(hs_ga* ga, int until, int finalize) {
@@ -148,12 +157,44 @@ int hs_ga_create_ex(hs_instance* h, const hs_ga_config* cfg, int islands, const 
     CK(cudaMalloc(&ga->out_order, (size_t)islands * h->k), "cudaMalloc");
     CK(cudaMalloc(&ga->out_groups, (size_t)islands * km * 2), "cudaMalloc");
     if (h->k > 8) CK(cudaMalloc(&ga->hk_scratch, (size_t)islands * hs::hk_big_size(h->k) * 8), "cudaMalloc");
+    // d_pp 9..16: a generation's snapshots (all islands) are priced together
+    // by the stage + cluster Held-Karp kernels (HS_GA_BATCH=0: in-kernel CTA
+    // pricing, one snapshot at a time)
+    const char* benv = getenv("HS_GA_BATCH");
+    if (h->k > 8 && h->two.rwords && !(benv && benv[0] == '0')) {
+        ga->batch = true;
+        ga->snap_stride = std::max(cfg->pop_size, 1 + cfg->max_passes);
+        const size_t slots = (size_t)islands * ga->snap_stride;
+        CK(cudaMalloc(&ga->snap_buf, slots * km * 2), "cudaMalloc");
+        CK(cudaMalloc(&ga->snap_cost, slots * 8), "cudaMalloc");
+        CK(cudaMalloc(&ga->snap_cnt, (size_t)islands * 4), "cudaMalloc");
+        CK(cudaMalloc(&ga->invalid, 4), "cudaMalloc");
+    }
     CK(cudaMemcpy(ga->state, st.data(), sizeof(hs::GAState) * islands, cudaMemcpyHostToDevice), "upload state");
     if (getenv("HS_GA_PROFILE")) {
         CK(cudaMalloc(&ga->prof, 16 * sizeof(long long)), "cudaMalloc");
         CK(cudaMemset(ga->prof, 0, 16 * sizeof(long long)), "memset");
     }
     *out = ga;
+    return 0;
+}
+
+// One batch-priced step: phase 1 (snapshots out), the stage + cluster
+// Held-Karp pricing of every island's slots, phase 2 (commit).
+static int ga_batch_step(hs_ga* ga, int until, bool key16, cudaStream_t st) {
+    hs::GAArgs a = ga_args(ga, until, 0);
+    a.snap_stride = ga->snap_stride;
+    a.snap_buf = ga->snap_buf;
+    a.snap_cost = ga->snap_cost;
+    a.snap_cnt = ga->snap_cnt;
+    a.phase = 1;
+    if (hs::launch_ga(a, ga->plan, ga->islands, key16, st)) return fail(-1, "ga emit launch", cudaGetLastError());
+    const int64_t P = (int64_t)ga->islands * ga->snap_stride;
+    if (int rc = hs_eval_batch(ga->h, ga->snap_buf, P, ga->snap_cost, nullptr, nullptr, nullptr, nullptr, ga->invalid,
+                               st))
+        return rc;
+    a.phase = 2;
+    if (hs::launch_ga(a, ga->plan, ga->islands, key16, st)) return fail(-1, "ga commit launch", cudaGetLastError());
     return 0;
 }
 
@@ -164,6 +205,20 @@ int hs_ga_run(hs_ga* ga, int until, void* stream) {
     until = std::min(until, ga->cfg.generations);
     cudaStream_t st = (cudaStream_t)stream;
     const bool key16 = ga->h->rank16 != nullptr;
+    if (ga->batch) {
+        if (!ga->started)
+            if (int rc = ga_batch_step(ga, 0, key16, st)) return rc;  // init_population + its pricing
+        ga->started = true;
+        for (; ga->host_gen < until; ga->host_gen++)
+            if (int rc = ga_batch_step(ga, ga->host_gen + 1, key16, st)) return rc;
+        if (until >= ga->cfg.generations) {  // canonical best of every island
+            hs::GAArgs af = ga_args(ga, until, 1);
+            if (hs::launch_ga(af, ga->plan, ga->islands, key16, st))
+                return fail(-1, "ga finalize launch", cudaGetLastError());
+        }
+        ga->last = st;
+        return 0;
+    }
     if (ga->spec < 0) {
         // one GA: generations as a speculative pipeline over a thread-block
         // cluster (hs_search_ga_spec.cu); HS_GA_SPEC=0 keeps the one-CTA kernel
@@ -271,7 +326,8 @@ int hs_ga_destroy(hs_ga* ga) {
     DeviceGuard dg(ga->h->device);
     for (void* p : {(void*)ga->state, (void*)ga->pop, (void*)ga->cost, (void*)ga->best, (void*)ga->trace_best,
                     (void*)ga->trace_mean, (void*)ga->out3, (void*)ga->out_pg, (void*)ga->out_order,
-                    (void*)ga->out_groups, (void*)ga->hk_scratch, (void*)ga->prof})
+                    (void*)ga->out_groups, (void*)ga->hk_scratch, (void*)ga->prof, (void*)ga->snap_buf,
+                    (void*)ga->snap_cost, (void*)ga->snap_cnt, (void*)ga->invalid})
         if (p) cudaFree(p);
     delete ga;
     return 0;

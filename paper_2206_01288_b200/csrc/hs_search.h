@@ -41,6 +41,16 @@ struct GAArgs {
     int8_t* out_order;   // [islands][k]
     int16_t* out_groups; // [islands][k*m] canonical best
     long long* prof;     // optional driver-phase cycle counters (island 0), see hs_search.cu
+    // batch-priced generations (d_pp 9..16 with the cluster Held-Karp path):
+    // phase 1 runs one generation up to its snapshots and writes them to
+    // snap_buf (island i: slots [i * snap_stride, + snap_cnt[i]), the rest
+    // marked invalid; the initial population on the first call), phase 2
+    // commits that generation from snap_cost; phase 0 prices in-kernel
+    int phase;
+    int snap_stride;
+    int16_t* snap_buf;   // [islands][snap_stride][k*m]
+    double* snap_cost;   // [islands][snap_stride] (totals)
+    int* snap_cnt;       // [islands]
 };
 
 struct RefineArgs {

@@ -193,12 +193,12 @@ __device__ __forceinline__ double row_seq_mean(const LS& s, int u, const int16_t
     const double* wr = s.W + (size_t)u * s.n;
     double r = 0.0;  // sequential: w[:, grp].mean(axis=1) reduces an F-contiguous array
     int i = 0;
-    for (; i + 4 <= cnt; i += 4) {
-        double w0 = wr[grp[i]], w1 = wr[grp[i + 1]], w2 = wr[grp[i + 2]], w3 = wr[grp[i + 3]];
-        r += w0;
-        r += w1;
-        r += w2;
-        r += w3;
+    for (; i + 8 <= cnt; i += 8) {  // eight loads in flight, added in order
+        double w[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) w[t] = wr[grp[i + t]];
+#pragma unroll
+        for (int t = 0; t < 8; t++) r += w[t];
     }
     for (; i < cnt; i++) r += wr[grp[i]];
     return div_count(r, cnt);
@@ -242,13 +242,25 @@ __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
             code = i * 256 + l;
         }
     } else {
-        for (int t = lane; t < c * c; t += kWarp) {
-            int i = t / c, l = t - (t / c) * c;
-            if (l <= i) continue;
-            double v = s.W[(size_t)g[i] * s.n + g[l]];
-            if (v < bv) {  // t ascends per lane, so strict < keeps the first
-                bv = v;
-                code = i * 256 + l;
+        // eight rows at a time, lanes over the partners l > i (32 per step):
+        // independent loads in flight; minimum by (value, code), so the
+        // lexicographically first pair wins ties whatever the visit order
+        for (int i0 = 0; i0 < c - 1; i0 += 8) {
+            for (int l0 = i0 + 1; l0 < c; l0 += kWarp) {
+                double v[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const int i = i0 + r, l = l0 + r + lane;
+                    v[r] = (i < c - 1 && l > i && l < c) ? s.W[(size_t)g[i] * s.n + g[l]] : kInf;
+                }
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const int cr = (i0 + r) * 256 + (l0 + r + lane);
+                    if (v[r] < bv || (v[r] == bv && cr < code)) {
+                        bv = v[r];
+                        code = cr;
+                    }
+                }
             }
         }
     }
@@ -285,6 +297,23 @@ __device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa,
         const int u = q == 0 ? d1 : q == 1 ? d2 : q == 2 ? d1p : d2p;
         const int16_t* gg = q < 2 ? gj2 : gj;
         double x = butterfly8(s.W[(size_t)u * s.n + gg[e]]);
+        S0 = __shfl_sync(kFull, x, 0);
+        S1 = __shfl_sync(kFull, x, 8);
+        S2 = __shfl_sync(kFull, x, 16);
+        S3 = __shfl_sync(kFull, x, 24);
+    } else if (cj >= 8 && cj2 >= 8 && cj <= 128 && cj2 <= 128) {
+        // numpy pairwise sums of the four rows, lanes 8q..8q+7: lane e keeps
+        // accumulator r_e (terms e, e + 8, ... in order), the xor butterfly
+        // is numpy's tree, the tail is added in order by every lane
+        const int q = lane >> 3, e = lane & 7;
+        const int u = q == 0 ? d1 : q == 1 ? d2 : q == 2 ? d1p : d2p;
+        const int16_t* gg = q < 2 ? gj2 : gj;
+        const int c = q < 2 ? cj2 : cj, full = c - c % 8;
+        const double* wr = s.W + (size_t)u * s.n;
+        double r = wr[gg[e]];
+        for (int i = 8 + e; i < full; i += 8) r += wr[gg[i]];
+        double x = butterfly8(r);
+        for (int i = full; i < c; i++) x += wr[gg[i]];
         S0 = __shfl_sync(kFull, x, 0);
         S1 = __shfl_sync(kFull, x, 8);
         S2 = __shfl_sync(kFull, x, 16);
@@ -635,8 +664,13 @@ __device__ inline void ensure_caches(LS& s, int lane) {
         for (int a = lane; a < c; a += kWarp) {
             const double* wr = s.W + (size_t)g[a] * n;
             double h = kInf;
-            for (int b = 0; b < c; b++)
-                if (b != a) h = dmin(h, wr[g[b]]);
+            for (int b0 = 0; b0 < c; b0 += 8) {  // eight independent loads in flight (min is order-free)
+                double x[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++) x[t] = (b0 + t < c && b0 + t != a) ? wr[g[b0 + t]] : kInf;
+#pragma unroll
+                for (int t = 0; t < 8; t++) h = dmin(h, x[t]);
+            }
             s.home[g[a]] = h;
         }
     }
@@ -1577,10 +1611,21 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     if (driver) rng.load(st.rng);
     if (a.prof && isl == 0 && threadIdx.x == 0) g_prof = a.prof;
 
+    const bool st_was_init = st.initialized;
+    int16_t* isnap = a.snap_buf ? a.snap_buf + (size_t)isl * a.snap_stride * km : nullptr;
+    // phase 1: hand slots [cnt, snap_stride) over as invalid layouts (the
+    // batch pricer skips them)
+    auto emit_pad = [&](int cnt) {
+        if (driver) {
+            for (int q = cnt + lane; q < a.snap_stride; q += kWarp) isnap[(size_t)q * km] = -1;
+            if (lane == 0) a.snap_cnt[isl] = cnt;
+        }
+    };
+    bool emitted = false;
     if (!st.initialized) {
         // init_population (scheduler.py:124-136): sequential random_partition
         // draws, then price every member (:537-542)
-        if (driver) {
+        if (driver && a.phase != 2) {
             for (int i = 0; i < P; i++) {
                 int16_t* dst = g.snaps;  // scratch
                 if (lane == 0) {
@@ -1612,16 +1657,26 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         }
         __threadfence_block();
         island_sync();
-        // price the population in chunks of max_snaps through smem
-        for (int c0 = 0; c0 < P; c0 += max_snaps) {
-            int cnt = min(max_snaps, P - c0);
+        if (a.phase == 1) {  // the population goes out for batch pricing
+            if (driver) copy16(isnap, pop, P * km, lane);
+            emit_pad(P);
+            emitted = true;
+        } else if (a.phase == 2) {
             const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
-            for (int t = t0; t < cnt * km; t += dt) g.snaps[t] = pop[(size_t)c0 * km + t];
+            for (int t = t0; t < P; t += dt) g.popcost[t] = a.snap_cost[(size_t)isl * a.snap_stride + t];
             island_sync();
-            pr.all(g.snaps, cnt, km, g.popcost + c0, pw, pW, lane);
-            island_sync();
+        } else {
+            // price the population in chunks of max_snaps through smem
+            for (int c0 = 0; c0 < P; c0 += max_snaps) {
+                int cnt = min(max_snaps, P - c0);
+                const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+                for (int t = t0; t < cnt * km; t += dt) g.snaps[t] = pop[(size_t)c0 * km + t];
+                island_sync();
+                pr.all(g.snaps, cnt, km, g.popcost + c0, pw, pW, lane);
+                island_sync();
+            }
         }
-        if (driver) {
+        if (driver && !emitted) {
             if (lane == 0) {
                 int bi = 0;
                 for (int i = 1; i < P; i++)
@@ -1648,14 +1703,16 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
     __threadfence_block();
     island_sync();
 
-    const int gen_end = min(a.gen_end, a.generations);
+    // an emitted initial population, or its commit, runs no generation
+    const bool init_call = emitted || (a.phase == 2 && !st_was_init);
+    const int gen_end = init_call ? 0 : min(a.gen_end, a.generations);
     const int stop_after = a.kind == 0 ? 2 : 1;
     // CTA-mode islands with the register sweep path run the even passes as
     // waves over all warps (balanced groups are checked per pass below)
     const bool waves = !kWI && !kCta && a.kind == 0 && m == 8 && n <= 128 && W > 1;
     while (!g.ctl[1] && g.ctl[2] < gen_end) {
         const int gen = g.ctl[2];
-        if (driver) {
+        if (driver && a.phase != 2) {
             int i = 0, i2 = 0;
             if (lane == 0) {
                 i = (int)rng.integers(0, P);
@@ -1697,7 +1754,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             if (waves) load_groups(s, g.snaps, lane);
             if (lane == 0) g.ctl[0] = nsnap;
         }
-        if (waves) {
+        if (waves && a.phase != 2) {
             // _refine with the even passes spread over the CTA's warps; the
             // odd passes (chains) stay on the driver warp
             island_sync();
@@ -1732,8 +1789,22 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         }
         long long q0 = clock64();
         island_sync();
+        if (a.phase == 1) {  // this generation's snapshots go out for batch pricing
+            const int ns = g.ctl[0];
+            if (driver) copy16(isnap, g.snaps, ns * km, lane);
+            emit_pad(ns);
+            emitted = true;
+            break;
+        }
+        if (a.phase == 2 && driver && lane == 0) g.ctl[0] = a.snap_cnt[isl];
+        island_sync();
         const int nsnap = g.ctl[0];
-        pr.all(g.snaps, nsnap, km, g.snapcost, pw, pW, lane);
+        if (a.phase == 2) {
+            const int t0 = kWI ? lane : threadIdx.x, dt = kWI ? kWarp : blockDim.x;
+            for (int t = t0; t < nsnap; t += dt) g.snapcost[t] = a.snap_cost[(size_t)isl * a.snap_stride + t];
+        } else {
+            pr.all(g.snaps, nsnap, km, g.snapcost, pw, pW, lane);
+        }
         island_sync();
         if (a.prof && isl == 0 && lane == 0 && driver) a.prof[3] += clock64() - q0;
         if (driver) {
@@ -1760,7 +1831,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
             worst = __shfl_sync(kFull, worst, 0);
             replace = __shfl_sync(kFull, replace, 0);
             improve = __shfl_sync(kFull, improve, 0);
-            const int16_t* refined = g.snaps + (size_t)bsi * km;
+            const int16_t* refined = (a.phase == 2 ? isnap : g.snaps) + (size_t)bsi * km;
             if (replace) copy16(pop + (size_t)worst * km, refined, km, lane);
             if (improve) copy16(gbest, refined, km, lane);
             __syncwarp();
@@ -1777,7 +1848,9 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         }
         __threadfence_block();
         island_sync();
+        if (a.phase == 2) break;  // one generation per commit
     }
+    if (a.phase == 1 && !emitted) emit_pad(0);  // stopped or done: nothing to price
 
     // persist population costs; finalize when the run is over
     {
@@ -1785,7 +1858,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         for (int t = t0; t < P; t += dt) gcost[t] = g.popcost[t];
     }
     bool finished = g.ctl[1] || g.ctl[2] >= a.generations;
-    if (finished && a.finalize && !st.finalized) {
+    if (finished && a.finalize && !st.finalized && a.phase == 0) {
         // canonical() (costmodel.py:86-88) then a last priced evaluation (:572-574)
         if (driver && lane == 0) {
             int ord[16];

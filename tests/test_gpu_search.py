@@ -230,6 +230,50 @@ def test_evolve_d_pp_above_8_vs_oracle(name, kind, pop, gens):
     assert [t[2] for t in r.trace] == list(o["trace_mean"])
 
 
+@pytest.mark.parametrize("name,kind,patience", [("r32_16x2", "ours", None), ("r48_12x4", "kl", 3),
+                                                 ("r18_9x2", "ours", 4)])
+def test_batch_priced_islands_d_pp_above_8_vs_oracle(name, kind, patience):
+    """d_pp 9..16 islands with batch-priced generations (every island's
+    snapshots of a generation priced together by the stage + cluster
+    Held-Karp kernels), run in epochs, == independent oracle evolve runs."""
+    g, w = I.instance(name)
+    cfg = S.ScheduleConfig(pop_size=8, generations=10, local_search=kind, patience=patience)
+    rngs = S.island_seeds(11, 12)
+    states = [O.PCG64State.from_generator(r) for r in S.island_seeds(11, 12)]
+    sess = S.GASession(g, w, cfg, rngs)
+    for until in (3, 4, 10):
+        sess.run(until)
+    res = sess.results()
+    orc = O.Oracle.of(g, w)
+    for i, r in enumerate(res):
+        o = orc.evolve(cfg.pop_size, cfg.generations, kind, state=states[i], patience=patience)
+        assert [list(x) for x in r.best_partition.groups] == o["partition"].tolist()
+        assert r.best_cost.total == o["total"] and r.evaluations == o["evaluations"]
+        assert [t[1] for t in r.trace] == list(o["trace_best"])
+        assert [t[2] for t in r.trace] == list(o["trace_mean"])
+        assert O.PCG64State.from_generator(rngs[i]).as_tuple() == states[i].as_tuple()
+
+
+def test_batch_priced_generations_equal_in_kernel_pricing(monkeypatch):
+    """HS_GA_BATCH=0 (each island prices its snapshots in-kernel, one at a
+    time) and the batch-priced generations give identical sessions,
+    migration included."""
+    g, w = I.instance("r32_16x2")
+    cfg = S.ScheduleConfig(pop_size=8, generations=6, local_search="ours")
+
+    def run():
+        sess = S.GASession(g, w, cfg, S.island_seeds(2, 6))
+        for epoch in range(2):
+            sess.run(3 * (epoch + 1))
+            gr, co = sess.export_elites(2)
+            sess.import_elites(gr, co, [(i - 1) % 6 for i in range(6)])
+        return [r.to_dict() for r in sess.results()]
+
+    batched = run()
+    monkeypatch.setenv("HS_GA_BATCH", "0")
+    assert run() == batched
+
+
 def test_local_search_d_pp_16_vs_oracle():
     g, w = I.instance("r32_16x2")
     rng = np.random.default_rng(1)
