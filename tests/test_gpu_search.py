@@ -216,9 +216,11 @@ def test_evolve_errors_like_reference():
 
 @pytest.mark.parametrize("name,kind,pop,gens", [("r32_16x2", "ours", 8, 12), ("r32_16x2", "kl", 8, 12),
                                                 ("r48_12x4", "ours", 8, 6), ("r18_9x2", "ours", 8, 15),
-                                                ("config4", "kl", 4, 2)])
+                                                ("config4", "kl", 4, 2), ("config4", "ours", 4, 3),
+                                                ("r64_2x32", "ours", 8, 12)])
 def test_evolve_d_pp_above_8_vs_oracle(name, kind, pop, gens):
-    """GA with CTA-level pricing (d_pp 9..16) reproduces the oracle's evolve."""
+    """GA with CTA-level pricing (d_pp 9..16) or 32-member groups (the
+    incremental fast-edge path) reproduces the oracle's evolve."""
     g, w = I.instance(name)
     cfg = S.ScheduleConfig(pop_size=pop, generations=gens, local_search=kind, seed=4)
     r = S.evolve(g, w, cfg)
