@@ -555,6 +555,14 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     if (!h->chunk) {
         h->chunk = 1 << 16;  // 8 MB of layouts per H2D chunk (measured best for e2e: 2^14..2^20 swept)
         if (const char* e = getenv("HS_HOST_CHUNK_LOG2")) h->chunk = (int64_t)1 << std::max(10, std::min(24, atoi(e)));
+        hs::EvalArgs probe = base_args(h);
+        probe.groups = nullptr;  // 16-byte aligned by construction (cudaMalloc)
+        if (hs::eval8_applicable(probe, h->smem_optin)) {
+            // whole waves of the eval8 kernel per chunk: every warp gets the
+            // same number of quads, no half-empty last iteration per launch
+            const int64_t wave = hs::eval8_wave(h->sm_count);
+            h->chunk = std::max<int64_t>(1, (h->chunk + wave / 2) / wave) * wave;
+        }
         for (int i = 0; i < 2; i++) {
             CK(cudaMalloc(&h->cg[i], (size_t)h->chunk * km * 2), "cudaMalloc chunk");
             CK(cudaMalloc(&h->co[i], (size_t)h->chunk * (3 + h->k) * 8 + (size_t)h->chunk * h->k), "cudaMalloc chunk");

@@ -66,6 +66,7 @@ int launch_eval(const EvalArgs& a, const EvalPlan& plan, cudaStream_t s);
 // paper shape (8 x 8, N = 64, u16 keys, no stage order): four candidates per warp
 bool eval8_applicable(const EvalArgs& a, size_t smem_optin);
 int launch_eval8(const EvalArgs& a, int sm_count, cudaStream_t s);
+int64_t eval8_wave(int sm_count);
 int launch_bottleneck_batch(const double* w, int m, int64_t B, double* out, cudaStream_t s);
 int launch_narrow(int64_t nn, const uint32_t* src, uint16_t* dst, cudaStream_t s);
 int launch_path_batch(const double* w, int k, int64_t B, const HKTables& t, double* total, int8_t* order,
