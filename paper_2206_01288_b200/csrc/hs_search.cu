@@ -44,6 +44,7 @@ __global__ void crossover_kernel(int n, int k, int m, const int16_t* p1, const i
     s.cap = cap;
     s.W = nullptr;
     s.w_sh = 0;
+    s.lat = false;
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(32) pass_kernel(PassArgs a) {
     s.cap = cap;
     s.W = a.sw;
     s.w_sh = 0;
+    s.lat = false;
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = a.mean + (size_t)b * n * k;

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
     s.cap = cap;
     s.W = SW;
     s.w_sh = kSmemTables ? (uint32_t)__cvta_generic_to_shared(SW) : 0u;
+    s.lat = true;
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));

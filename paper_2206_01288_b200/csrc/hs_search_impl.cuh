@@ -68,6 +68,7 @@ struct LS {
     int n, k, m, cap;
     const double* W;  // surrogate weights n x n (scheduler.py:84-88)
     uint32_t w_sh;    // shared-window address of W when it was staged in shared memory, else 0
+    bool lat;         // latency regime: one working warp per SM (CTA islands, refine, spec workers)
     int16_t* G;       // k x cap members, ascending
     int* sz;          // k sizes
     double* mean;     // n x k: mean[u*k+i] = seq_sum(W[u, G_i]) / sz_i, computed lazily
@@ -664,12 +665,17 @@ __device__ inline void ensure_caches(LS& s, int lane) {
         for (int a = lane; a < c; a += kWarp) {
             const double* wr = s.W + (size_t)g[a] * n;
             double h = kInf;
-            for (int b0 = 0; b0 < c; b0 += 8) {  // eight independent loads in flight (min is order-free)
-                double x[8];
+            if (s.lat) {  // one driver warp per SM: eight loads in flight (min is order-free)
+                for (int b0 = 0; b0 < c; b0 += 8) {
+                    double x[8];
 #pragma unroll
-                for (int t = 0; t < 8; t++) x[t] = (b0 + t < c && b0 + t != a) ? wr[g[b0 + t]] : kInf;
+                    for (int t = 0; t < 8; t++) x[t] = (b0 + t < c && b0 + t != a) ? wr[g[b0 + t]] : kInf;
 #pragma unroll
-                for (int t = 0; t < 8; t++) h = dmin(h, x[t]);
+                    for (int t = 0; t < 8; t++) h = dmin(h, x[t]);
+                }
+            } else {  // many warps per SM hide the latency; fewer instructions win
+                for (int b = 0; b < c; b++)
+                    if (b != a) h = dmin(h, wr[g[b]]);
             }
             s.home[g[a]] = h;
         }
@@ -1569,6 +1575,7 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         s.cap = cap;
         s.W = SW;
         s.w_sh = kSmemTables ? (uint32_t)__cvta_generic_to_shared(SW) : 0u;
+        s.lat = !kWI;
         s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
         s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
         s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
@@ -1934,6 +1941,7 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     s.cap = cap;
     s.W = SW;
     s.w_sh = kSmemTables ? (uint32_t)__cvta_generic_to_shared(SW) : 0u;
+    s.lat = true;
     s.G = reinterpret_cast<int16_t*>(take((size_t)k * cap * 2));
     s.sz = reinterpret_cast<int*>(take((size_t)k * 4));
     s.mean = reinterpret_cast<double*>(take((size_t)n * k * 8));
