@@ -370,6 +370,8 @@ def run_ours():
     }
     if not ARGS.no_ga:
         line["ga"] = ga_legs(g, w, rank, world, local, barrier, dist)
+    if not ARGS.no_sweep:
+        line["config4_island_model"] = config4_island_leg(rank, world, local, barrier, dist)
     if not ARGS.no_sweep and world == 1:
         line["other_configs"] = sweep_legs(local)
     if rank == 0 and world == 1 and not ARGS.no_cpu_baseline:
@@ -485,6 +487,53 @@ def ga_legs(g, w, rank, world, local, barrier, dist):
     return out
 
 
+def config4_island_leg(rank, world, local, barrier, dist):
+    """BASELINE config 4's island model: 512 devices, d_pp = 16 x d_dp = 32,
+    one CTA island per SM on every GPU (generations batch-priced by the
+    stage + cluster Held-Karp kernels), one elite per island migrating
+    around the global ring over NCCL every 2 generations; time = max over
+    ranks, evaluations from the islands' own counters."""
+    import torch
+    from paper_2206_01288_b200 import scheduler as S
+    from paper_2206_01288_b200.netmodel import config4_scenario
+    from paper_2206_01288_b200.workload import WorkloadSpec
+
+    g4 = config4_scenario().graph()
+    w4 = WorkloadSpec(16, 32, 268_435_456, 201_326_592)
+    icfg = S.ScheduleConfig(pop_size=16, generations=6, local_search="ours", seed=5)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    r = dist.get_rank() if world > 1 else 0
+    src = S.migration_sources(r, world, sms)
+    sess = S.GASession(g4, w4, icfg, S.island_seeds(icfg.seed, sms, offset=r * sms))
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    gen = 0
+    while gen < icfg.generations:
+        gen = min(icfg.generations, gen + 2)
+        sess.run(gen)
+        if gen < icfg.generations:
+            gr, co = sess.export_elites(1)
+            all_gr, all_co = S.gather_elites(gr, co)
+            sess.import_elites(all_gr, all_co, src)
+    res = sess.results()
+    torch.cuda.synchronize()
+    barrier()
+    tt = torch.tensor([time.perf_counter() - t0, float(sum(x.evaluations for x in res))], dtype=torch.float64,
+                      device=f"cuda:{local}")
+    if world > 1:
+        t_max = tt[:1].clone()
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        tt[0] = t_max[0]
+    t_isl, evals = float(tt[0].item()), float(tt[1].item())
+    return {"islands": sms * world, "gpus": world, "generations": icfg.generations, "pop_size": icfg.pop_size,
+            "seconds": t_isl, "island_generations_per_s": sms * world * icfg.generations / t_isl,
+            "evals_per_s": evals / t_isl,
+            "migration": "1 elite per island every 2 generations, global ring, NCCL all-gather",
+            "what": "one CTA island per SM per GPU, 512 devices 16x32, ours, incl. init pricing, time max over ranks"}
+
+
 def sweep_legs(local):
     """Device-resident evals/s on the other BASELINE configs (reported beside
     the headline, not as bench lines): config 3 = the five paper scenarios
@@ -539,21 +588,6 @@ def sweep_legs(local):
     g4 = config4_scenario().graph()
     w4 = WorkloadSpec(16, 32, 268_435_456, 201_326_592)
     out["config4_512dev_16x32_evals_per_s"] = rate(g4, w4, 16384, reps=2)
-    # config 4's "island model": one GA island per SM (CTA islands, d_pp = 16
-    # pricing inside the GA kernel), a few generations; evaluations counted
-    # from the islands' own results
-    icfg = S.ScheduleConfig(pop_size=16, generations=3, local_search="ours", seed=5)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    sess = S.GASession(g4, w4, icfg, S.island_seeds(icfg.seed, sms))
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    sess.run(icfg.generations)
-    res = sess.results()
-    t_isl = time.perf_counter() - t0
-    out["config4_islands"] = {"islands": sms, "generations": icfg.generations, "pop_size": icfg.pop_size,
-                              "seconds": t_isl, "island_generations_per_s": sms * icfg.generations / t_isl,
-                              "evals_per_s": sum(r.evaluations for r in res) / t_isl,
-                              "what": "one CTA island per SM, 512 devices 16x32, ours, incl. init pricing"}
     g5 = random_graph(0, 1024)
     out["config5_1024dev_16x64_evals_per_s"] = rate(g5, WorkloadSpec(16, 64, 1 << 30, 3 << 26), 1024, reps=2)
     out["config5_1024dev_32x32_heuristic_evals_per_s"] = rate(g5, WorkloadSpec(32, 32, 1 << 30, 3 << 26), 4096,
