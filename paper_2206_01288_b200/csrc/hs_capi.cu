@@ -16,6 +16,8 @@
 #include "../../include/hetsched_b200.h"
 #include "hs_big.h"
 #include "hs_eval.cuh"
+#include <cuda.h>
+
 #include "hs_instance.h"
 
 namespace hsx {
@@ -470,7 +472,13 @@ int hs_instance_destroy(hs_instance* h) {
         if (h->co[i]) cudaFree(h->co[i]);
         if (h->cs[i]) cudaStreamDestroy(h->cs[i]);
     }
+    if (h->cup) cudaStreamDestroy(h->cup);
+    if (h->cdown) cudaStreamDestroy(h->cdown);
+    for (cudaEvent_t e : h->ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->ev_out) cudaEventDestroy(e);
     if (h->cinv) cudaFree(h->cinv);
+    if (h->arrived) cudaFree(h->arrived);
+    if (h->finished) cudaFree(h->finished);
     delete h;
     return 0;
 }
@@ -543,6 +551,31 @@ int hs_path_heuristic_batch(const double* w, int k, int64_t B, double* total, in
     return 0;
 }
 
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
+// entry points (no link-time libcuda dependency); null if unavailable
+namespace {
+using PFN_val32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamMemOps {
+    PFN_val32 write = nullptr, wait = nullptr;
+};
+const StreamMemOps& stream_mem_ops() {
+    static StreamMemOps ops = [] {
+        StreamMemOps o;
+        cudaDriverEntryPointQueryResult q1{}, q2{};
+        void *w = nullptr, *t = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+            o.write = reinterpret_cast<PFN_val32>(w);
+            o.wait = reinterpret_cast<PFN_val32>(t);
+        }
+        cudaGetLastError();
+        return o;
+    }();
+    return ops;
+}
+}  // namespace
+
 int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
                        double* pipelinep, double* per_group, int8_t* order, int32_t* invalid) {
     if (!h) return fail(-2, "null handle");
@@ -552,59 +585,183 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     std::lock_guard<std::mutex> lk(h->mu);
     DeviceGuard dg(h->device);
     const int km = h->k * h->m;
+    // Decoupled pipeline over a span of up to 2^22 layouts held on the
+    // device: all H2D chunk copies back to back on one copy stream (the host
+    // link never waits for a kernel), D2H copies on a third stream.  Streamed
+    // (eval8, 8x8 at N = 64): ONE kernel per span consumes the chunks as the
+    // copy stream announces them (cuStreamWriteValue32 behind each H2D) and
+    // counts finished quads per chunk, which the D2H stream waits on
+    // (cuStreamWaitValue32).  Otherwise one launch per chunk on alternating
+    // compute streams (a launch backfills the previous one's tail), ordered
+    // by events.
+    constexpr int64_t kSpan = (int64_t)1 << 22;
     if (!h->chunk) {
-        h->chunk = 1 << 16;  // 8 MB of layouts per H2D chunk (measured best for e2e: 2^14..2^20 swept)
+        h->chunk = 1 << 16;  // layouts per kernel launch (measured best for e2e: 2^14..2^20 swept)
         if (const char* e = getenv("HS_HOST_CHUNK_LOG2")) h->chunk = (int64_t)1 << std::max(10, std::min(24, atoi(e)));
         hs::EvalArgs probe = base_args(h);
         probe.groups = nullptr;  // 16-byte aligned by construction (cudaMalloc)
         if (hs::eval8_applicable(probe, h->smem_optin)) {
-            // whole waves of the eval8 kernel per chunk: every warp gets the
-            // same number of quads, no half-empty last iteration per launch
+            // whole waves of the eval8 kernel per launch: every warp gets the
+            // same number of quads, no half-empty last iteration
             const int64_t wave = hs::eval8_wave(h->sm_count);
             h->chunk = std::max<int64_t>(1, (h->chunk + wave / 2) / wave) * wave;
         }
-        for (int i = 0; i < 2; i++) {
-            CK(cudaMalloc(&h->cg[i], (size_t)h->chunk * km * 2), "cudaMalloc chunk");
-            CK(cudaMalloc(&h->co[i], (size_t)h->chunk * (3 + h->k) * 8 + (size_t)h->chunk * h->k), "cudaMalloc chunk");
-            CK(cudaStreamCreateWithFlags(&h->cs[i], cudaStreamNonBlocking), "stream");
-        }
+        // streamed path: one kernel per span, so the chunk only sets the
+        // grain of the copy / announce / D2H pipeline (measured best 2^15 of
+        // 2^13..2^17: 2.88e8 e2e at P = 2^20)
+        h->schunk = (int64_t)1 << 15;
+        if (const char* e = getenv("HS_HOST_CHUNK_LOG2")) h->schunk = (int64_t)1 << std::max(10, std::min(24, atoi(e)));
+        for (int i = 0; i < 2; i++) CK(cudaStreamCreateWithFlags(&h->cs[i], cudaStreamNonBlocking), "stream");
+        CK(cudaStreamCreateWithFlags(&h->cup, cudaStreamNonBlocking), "stream");
+        CK(cudaStreamCreateWithFlags(&h->cdown, cudaStreamNonBlocking), "stream");
         CK(cudaMalloc(&h->cinv, sizeof(int)), "cudaMalloc");
     }
-    CK(cudaMemsetAsync(h->cinv, 0, sizeof(int), h->cs[0]), "memset");
-    CK(cudaStreamSynchronize(h->cs[0]), "sync");
+    const int64_t span = std::min<int64_t>(P, kSpan);
+    if (span > h->span) {
+        if (h->cg[0]) cudaFree(h->cg[0]);
+        if (h->co[0]) cudaFree(h->co[0]);
+        h->cg[0] = nullptr;
+        h->co[0] = nullptr;
+        h->span = 0;
+        CK(cudaMalloc(&h->cg[0], (size_t)span * km * 2), "cudaMalloc host-path inputs");
+        CK(cudaMalloc(&h->co[0], (size_t)span * (3 + h->k) * 8 + (size_t)span * h->k), "cudaMalloc host-path outputs");
+        h->span = span;
+    }
+    const StreamMemOps& ops = stream_mem_ops();
+    hs::EvalArgs probe8 = base_args(h);
+    probe8.groups = h->cg[0];
+    const char* senv = getenv("HS_HOST_STREAMED");
+    const bool streamed = ops.write && ops.wait && !order && hs::eval8_applicable(probe8, h->smem_optin) &&
+                          !(senv && senv[0] == '0');
+    const int64_t chunk = streamed ? h->schunk : h->chunk;
+    const int64_t nch_max = (span + chunk - 1) / chunk + 2;  // chunks per span (first and last small)
+    while ((int64_t)h->ev_in.size() < nch_max) {
+        cudaEvent_t e1, e2;
+        CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
+        CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming), "event");
+        h->ev_in.push_back(e1);
+        h->ev_out.push_back(e2);
+    }
+    if (streamed && h->nslots < nch_max) {
+        if (h->arrived) cudaFree(h->arrived);
+        if (h->finished) cudaFree(h->finished);
+        h->arrived = nullptr;
+        h->finished = nullptr;
+        h->nslots = 0;
+        CK(cudaMalloc(&h->arrived, (size_t)nch_max * 4), "cudaMalloc");
+        CK(cudaMalloc(&h->finished, (size_t)nch_max * 4), "cudaMalloc");
+        CK(cudaMemset(h->arrived, 0, (size_t)nch_max * 4), "memset");
+        CK(cudaMemset(h->finished, 0, (size_t)nch_max * 4), "memset");
+        h->fin_target.assign((size_t)nch_max, 0u);
+        h->epoch = 0;
+        h->nslots = nch_max;
+    }
+    CK(cudaMemsetAsync(h->cinv, 0, sizeof(int), h->cup), "memset");
     hs::EvalArgs a = base_args(h);
     a.invalid = h->cinv;
-    // double-buffered chunks on two streams; the first chunk is small so the
-    // only copy not hidden behind a kernel is short
-    int64_t lo = 0;
-    for (int64_t c = 0; lo < P; c++) {
-        int b = (int)(c & 1);
-        cudaStream_t s = h->cs[b];
-        // ramp: a small first chunk (short exposed H2D) and a small last one
-        // (short exposed D2H); full chunks in between
-        const int64_t small = h->chunk / 8, left = P - lo;
-        int64_t cnt = c == 0 ? small : h->chunk;
-        if (c > 0 && left > small && left <= h->chunk + small) cnt = left - small;
-        cnt = std::min<int64_t>(cnt, left);
-        CK(cudaMemcpyAsync(h->cg[b], groups + lo * km, (size_t)cnt * km * 2, cudaMemcpyHostToDevice, s), "H2D");
-        a.groups = h->cg[b];
-        a.P = cnt;
-        a.total = h->co[b];
-        a.datap = h->co[b] + h->chunk;
-        a.pipe = h->co[b] + 2 * h->chunk;
-        a.per_group = per_group ? h->co[b] + 3 * h->chunk : nullptr;
-        a.order = order ? reinterpret_cast<int8_t*>(h->co[b] + (3 + h->k) * h->chunk) : nullptr;
-        int rc = launch_any(h, a, s);
-        if (rc) return rc;
-        CK(cudaMemcpyAsync(total + lo, a.total, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
-        if (datap) CK(cudaMemcpyAsync(datap + lo, a.datap, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
-        if (pipelinep) CK(cudaMemcpyAsync(pipelinep + lo, a.pipe, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
-        if (per_group)
-            CK(cudaMemcpyAsync(per_group + lo * h->k, a.per_group, (size_t)cnt * h->k * 8, cudaMemcpyDeviceToHost, s),
-               "D2H");
-        if (order) CK(cudaMemcpyAsync(order + lo * h->k, a.order, (size_t)cnt * h->k, cudaMemcpyDeviceToHost, s), "D2H");
-        lo += cnt;
+    const int64_t S = h->span;
+    double* const o_total = h->co[0];
+    double* const o_datap = o_total + S;
+    double* const o_pipe = o_total + 2 * S;
+    double* const o_pg = o_total + 3 * S;
+    int8_t* const o_order = reinterpret_cast<int8_t*>(o_total + (3 + h->k) * S);
+    for (int64_t base = 0; base < P; base += S) {
+        const int64_t n = std::min<int64_t>(S, P - base);
+        if (base) CK(cudaStreamSynchronize(h->cdown), "sync");  // the span's buffers are free again
+        // chunk plan: a small first chunk (short exposed H2D), a small last
+        // one (short exposed D2H), full chunks between
+        std::vector<std::pair<int64_t, int64_t>> ch;
+        for (int64_t lo = 0; lo < n;) {
+            const int64_t small = std::max<int64_t>(4, chunk / 8 / 4 * 4), left = n - lo;
+            int64_t cnt = ch.empty() ? small : chunk;
+            if (!streamed && !ch.empty() && left > small && left <= chunk + small) cnt = left - small;
+            cnt = std::min<int64_t>(cnt, left);
+            ch.emplace_back(lo, cnt);
+            lo += cnt;
+        }
+        if (streamed) {
+            // one kernel for the span: chunk c is announced by a value write
+            // behind its H2D copy, its D2H waits for the kernel's count of
+            // finished quads (no per-chunk launches, no tails between them)
+            // the kernel is enqueued first: it waits for its chunks on the GPU
+            const uint32_t ep = ++h->epoch;
+            a.groups = h->cg[0];
+            a.P = n;
+            a.total = o_total;
+            a.datap = o_datap;
+            a.pipe = o_pipe;
+            a.per_group = per_group ? o_pg : nullptr;
+            a.order = nullptr;
+            a.arrived = h->arrived;
+            a.finished = h->finished;
+            a.epoch = ep;
+            a.c0 = ch[0].second;
+            a.c = chunk;
+            if (int rc = launch_any(h, a, h->cs[0])) return rc;
+            a.arrived = nullptr;
+            a.finished = nullptr;
+            for (size_t c = 0; c < ch.size(); c++) {
+                const int64_t lo = ch[c].first, cnt = ch[c].second;
+                CK(cudaMemcpyAsync(h->cg[0] + lo * km, groups + (base + lo) * km, (size_t)cnt * km * 2,
+                                   cudaMemcpyHostToDevice, h->cup), "H2D");
+                if (ops.write(h->cup, (CUdeviceptr)(h->arrived + c), ep, 0) != CUDA_SUCCESS)
+                    return fail(-1, "cuStreamWriteValue32");
+            }
+            for (size_t c = 0; c < ch.size(); c++) {
+                const int64_t lo = ch[c].first, cnt = ch[c].second, g = base + lo;
+                cudaStream_t s = h->cdown;
+                h->fin_target[c] += (uint32_t)((cnt + 3) / 4);
+                if (ops.wait(s, (CUdeviceptr)(h->finished + c), h->fin_target[c], CU_STREAM_WAIT_VALUE_GEQ) !=
+                    CUDA_SUCCESS)
+                    return fail(-1, "cuStreamWaitValue32");
+                CK(cudaMemcpyAsync(total + g, o_total + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+                if (datap) CK(cudaMemcpyAsync(datap + g, o_datap + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+                if (pipelinep)
+                    CK(cudaMemcpyAsync(pipelinep + g, o_pipe + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+                if (per_group)
+                    CK(cudaMemcpyAsync(per_group + g * h->k, o_pg + lo * h->k, (size_t)cnt * h->k * 8,
+                                       cudaMemcpyDeviceToHost, s), "D2H");
+            }
+            continue;
+        }
+        for (size_t c = 0; c < ch.size(); c++) {
+            const int64_t lo = ch[c].first, cnt = ch[c].second;
+            CK(cudaMemcpyAsync(h->cg[0] + lo * km, groups + (base + lo) * km, (size_t)cnt * km * 2,
+                               cudaMemcpyHostToDevice, h->cup), "H2D");
+            CK(cudaEventRecord(h->ev_in[c], h->cup), "event");
+        }
+        for (size_t c = 0; c < ch.size(); c++) {
+            const int64_t lo = ch[c].first, cnt = ch[c].second;
+            cudaStream_t s = h->cs[c & 1];
+            CK(cudaStreamWaitEvent(s, h->ev_in[c], 0), "wait");
+            a.groups = h->cg[0] + lo * km;
+            a.P = cnt;
+            a.total = o_total + lo;
+            a.datap = o_datap + lo;
+            a.pipe = o_pipe + lo;
+            a.per_group = per_group ? o_pg + lo * h->k : nullptr;
+            a.order = order ? o_order + lo * h->k : nullptr;
+            int rc = launch_any(h, a, s);
+            if (rc) return rc;
+            CK(cudaEventRecord(h->ev_out[c], s), "event");
+        }
+        for (size_t c = 0; c < ch.size(); c++) {
+            const int64_t lo = ch[c].first, cnt = ch[c].second, g = base + lo;
+            cudaStream_t s = h->cdown;
+            CK(cudaStreamWaitEvent(s, h->ev_out[c], 0), "wait");
+            CK(cudaMemcpyAsync(total + g, o_total + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+            if (datap) CK(cudaMemcpyAsync(datap + g, o_datap + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+            if (pipelinep)
+                CK(cudaMemcpyAsync(pipelinep + g, o_pipe + lo, (size_t)cnt * 8, cudaMemcpyDeviceToHost, s), "D2H");
+            if (per_group)
+                CK(cudaMemcpyAsync(per_group + g * h->k, o_pg + lo * h->k, (size_t)cnt * h->k * 8,
+                                   cudaMemcpyDeviceToHost, s), "D2H");
+            if (order)
+                CK(cudaMemcpyAsync(order + g * h->k, o_order + lo * h->k, (size_t)cnt * h->k, cudaMemcpyDeviceToHost, s),
+                   "D2H");
+        }
     }
+    CK(cudaStreamSynchronize(h->cdown), "sync");
     CK(cudaStreamSynchronize(h->cs[0]), "sync");
     CK(cudaStreamSynchronize(h->cs[1]), "sync");
     if (invalid) CK(cudaMemcpy(invalid, h->cinv, sizeof(int), cudaMemcpyDeviceToHost), "D2H invalid");

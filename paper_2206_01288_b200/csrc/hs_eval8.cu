@@ -138,7 +138,7 @@ __device__ __forceinline__ E8Cand e8_load(const uint4* gsrc, int64_t p, bool liv
                                    (uint32_t)(8 * g + 4) | (uint32_t)(8 * g + 5) << 16,
                                    (uint32_t)(8 * g + 6) | (uint32_t)(8 * g + 7) << 16);
     E8Cand r;
-    r.gm = live ? __ldg(gsrc + p * 8 + g) : ident;
+    r.gm = live ? __ldcg(gsrc + p * 8 + g) : ident;  // L2 path: a streamed batch lands while the kernel runs
     int mem[8];
     mem[0] = i16(r.gm.x, 0), mem[1] = i16(r.gm.x, 1), mem[2] = i16(r.gm.y, 0), mem[3] = i16(r.gm.y, 1);
     mem[4] = i16(r.gm.z, 0), mem[5] = i16(r.gm.z, 1), mem[6] = i16(r.gm.w, 0), mem[7] = i16(r.gm.w, 1);
@@ -298,7 +298,35 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
 
     // latency mode: consecutive candidates on different CTAs (SMs) first
     const int64_t q0 = kC == 4 ? (int64_t)blockIdx.x * W + wid : (int64_t)wid * gridDim.x + blockIdx.x;
+    int64_t chunk = -1, done = 0;  // streamed batch: current chunk, quads finished in it
+    auto chunk_of = [&](int64_t q) { return q * kC < a.c0 ? 0 : 1 + (q * kC - a.c0) / a.c; };
+    auto report = [&]() {  // this warp is past `chunk`
+        if (chunk >= 0 && lane == 0) {
+            __threadfence();  // the chunk's outputs before its count
+            atomicAdd(a.finished + chunk, (uint32_t)done);
+        }
+    };
     for (int64_t q = q0; q * kC < a.P; q += (int64_t)gridDim.x * W) {
+        if (a.arrived) {
+            const int64_t ci = chunk_of(q);
+            if (ci != chunk) {
+                report();
+                chunk = ci;
+                done = 0;
+                if (lane == 0) {
+                    uint32_t v;
+                    const long long t0 = clock64();
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.arrived + ci) : "memory");
+                        if ((int32_t)(v - a.epoch) >= 0) break;
+                        if (clock64() - t0 > 40000000000LL) __trap();  // ~20 s: a chunk that never arrives fails the launch
+                        __nanosleep(256);
+                    }
+                }
+                __syncwarp();
+            }
+            done++;
+        }
         const int64_t p = q * kC + (kC == 4 ? c : 0);
         const bool live = (kC == 4 || c == 0) && p < a.P;
         const E8Cand cd = e8_load(gsrc, p, live, g, dp);
@@ -338,6 +366,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
         e8_out(a, p, live, g, cd.bad, cd.datap, pipe, cd.pg, kPerGroup);
         __syncwarp();
     }
+    if (a.arrived) report();
 }
 
 bool eval8_applicable(const EvalArgs& a, size_t smem_optin) {
@@ -364,6 +393,10 @@ int64_t eval8_wave(int sm_count) { return (int64_t)sm_count * kE8Warps * 4; }
 
 int launch_eval8(const EvalArgs& a, int sm_count, cudaStream_t s) {
     if (a.P == 0) return 0;
+    if (a.arrived) {  // streamed batch: the throughput kernel, whatever P
+        launch_eval8_c<4>(a, (int)std::min<int64_t>(sm_count, (a.P + 3) / 4), s);
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
     // small batches: one candidate per warp when the batch does not fill
     // the GPU's warps (a warp's latency is the floor), else four.  (Eight per
     // warp -- seven full matching rounds instead of 3.5 per quad -- cut the

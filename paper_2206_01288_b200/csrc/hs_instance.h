@@ -80,10 +80,22 @@ struct hs_instance {
     hs::EvalPlan plan{};
     // host-buffer path
     std::mutex mu;
-    int64_t chunk = 0;
-    int16_t* cg[2] = {nullptr, nullptr};
-    double* co[2] = {nullptr, nullptr};
+    int64_t chunk = 0;   // layouts per kernel launch (chunked path)
+    int64_t schunk = 0;  // layouts per announced chunk (streamed path)
+    int64_t span = 0;                 // layouts the host-path device buffers hold
+    int16_t* cg[2] = {nullptr, nullptr};  // [0]: inputs of a span (cg[1] unused)
+    double* co[2] = {nullptr, nullptr};   // [0]: outputs of a span (co[1] unused)
     int* cinv = nullptr;
-    cudaStream_t cs[2] = {nullptr, nullptr};
+    cudaStream_t cs[2] = {nullptr, nullptr};  // compute (alternating: a launch backfills the previous one's tail)
+    cudaStream_t cup = nullptr, cdown = nullptr;  // H2D / D2H copy streams
+    std::vector<cudaEvent_t> ev_in, ev_out;       // per chunk: inputs landed / outputs written
+    // streamed batches (eval8): one kernel per span consumes chunks as the
+    // copy stream's value writes announce them (epoch), and counts finished
+    // quads per chunk for the D2H stream's value waits
+    uint32_t* arrived = nullptr;
+    uint32_t* finished = nullptr;
+    std::vector<uint32_t> fin_target;
+    int64_t nslots = 0;
+    uint32_t epoch = 0;
 };
 

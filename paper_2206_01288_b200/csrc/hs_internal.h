@@ -45,6 +45,14 @@ struct EvalArgs {
     double* per_group;  // [P][k] or null
     int8_t* order;      // [P][k] or null
     int* invalid;       // count of malformed candidates
+    // streamed batch (eval8 only, null otherwise): the layouts arrive while
+    // the kernel runs, in chunks [0, c0), then c-sized ones; chunk i may be
+    // read once (int32)(arrived[i] - epoch) >= 0; each warp adds the quads it
+    // finished in chunk i to finished[i] (outputs fenced before)
+    const uint32_t* arrived;
+    uint32_t* finished;
+    uint32_t epoch;
+    int64_t c0, c;
 };
 
 struct EvalPlan {

@@ -157,6 +157,35 @@ def test_chunked_host_path_crosses_chunk_boundary():
     assert np.all(np.isfinite(r["total"]))
 
 
+@pytest.mark.parametrize("P", [1, 3, 4097, 36864, 100003])
+def test_streamed_host_path_equals_device_path(P):
+    """The host-buffer path at N = 64, 8x8 runs one kernel that consumes its
+    chunks as they land (stream value writes / waits): odd sizes, sizes
+    below one chunk, per-group outputs -- identical to the device path."""
+    import torch
+    g, w = I.instance("case4")
+    parts = _random_parts(40 + P % 7, P, 64, 8, 8)
+    host = hs.comm_cost_batch(g, parts, w, per_group=True)
+    dev = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w, per_group=True)
+    for key in host:
+        assert np.array_equal(host[key], dev[key].cpu().numpy()), key
+
+
+def test_host_path_spans_more_than_its_device_buffers():
+    """The host-buffer path holds up to 2^22 layouts on the device and runs
+    larger batches span by span: 2^22 + 4,321 tiled layouts price exactly
+    like their 997 distinct rows (oracle), in order, across the span seam."""
+    g, w = I.instance("case3")
+    uniq = _random_parts(31, 997, 64, 8, 8)
+    P = (1 << 22) + 4321
+    reps = -(-P // len(uniq))
+    parts = np.tile(uniq, (reps, 1, 1))[:P]
+    r = hs.comm_cost_batch(g, parts, w)
+    t, _, _ = O.Oracle.of(g, w).comm_cost_batch(uniq, threads=O.cpu_count())
+    want = np.tile(t, reps)[:P]
+    assert np.array_equal(r["total"], want)
+
+
 def test_malformed_partitions_raise():
     g, w = I.instance("case1")
     parts = _random_parts(1, 64, 64, 8, 8)
