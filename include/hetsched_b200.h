@@ -79,9 +79,11 @@ int hs_eval_batch(hs_instance *h, const int16_t *groups, int64_t P, double *tota
 int hs_eval_batch_ex(hs_instance *h, const int16_t *groups, int64_t P, double *total, double *datap, double *pipelinep,
                      double *per_group, int8_t *order, int32_t *invalid, int heuristic, void *stream);
 
-/* Same, host buffers (pinned for full overlap); copies in, evaluates in
- * double-buffered chunks, copies out, returns when done.  *invalid (host)
- * receives the malformed-candidate count. */
+/* Same, host buffers (pinned for full overlap); copies in, evaluates and
+ * copies out as a pipeline over device-held spans (at N = 64, 8x8 one kernel
+ * per span consumes chunks as they land), returns when done.  *invalid
+ * (host) receives the malformed-candidate count.  Replaces the per-layout
+ * comm_cost loop of scheduler.py:537-542 for host arrays. */
 int hs_eval_batch_host(hs_instance *h, const int16_t *groups, int64_t P, double *total, double *datap,
                        double *pipelinep, double *per_group, int8_t *order, int32_t *invalid);
 
