@@ -8,14 +8,16 @@
 //                     the coarsened stage graph -> E in global memory.
 //   hk_cluster_kernel one thread-block cluster per candidate: Held-Karp
 //                     (combinatorics.py:258-276) keeping only popcount layers
-//                     p-1 and p, each layer split over the cluster's CTAs'
-//                     shared memory; a cluster barrier separates layers.
-//                     Tasks are "pushed": the CTA holding h[r][.] computes
-//                     every h[r | u][u] from local reads and stores the one
-//                     result into the owning CTA's slice (DSMEM store, no
-//                     remote-load latency on the critical path).  At k = 16
-//                     the two live layers are 2 x 102,960 doubles (1.65 MB):
-//                     8 CTAs x 206 KB, so the table never leaves the SMs.
+//                     p-1 and p, each layer split by whole sets over the
+//                     cluster's CTAs' shared memory.  Work is "pushed": the
+//                     CTA owning r reads h[r][.] from its own shared memory
+//                     and sends every h[r | u][u] to the owner of r | u as an
+//                     asynchronous DSMEM store completing on that CTA's
+//                     mbarrier for the layer (st.async ... complete_tx); a
+//                     relaxed cluster barrier only guards buffer reuse.  At
+//                     k = 16 the two live layers are 2 x 102,960 doubles
+//                     (1.65 MB): 16 CTAs x 105 KB, two CTAs per SM, so the
+//                     table never leaves the SMs.
 // Values are the reference's: h[s][u] = min_v (w[u][v] + h[s\u][v]) with
 // strict '<' (the min of a set of doubles does not depend on visit order),
 // total = first minimum over the full set.  Stage orders still use the
