@@ -576,14 +576,8 @@ const StreamMemOps& stream_mem_ops() {
 }
 }  // namespace
 
-int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
-                       double* pipelinep, double* per_group, int8_t* order, int32_t* invalid) {
-    if (!h) return fail(-2, "null handle");
-    if (P < 0) return fail(-2, "negative batch");
-    if (invalid) *invalid = 0;
-    if (P == 0) return 0;
-    std::lock_guard<std::mutex> lk(h->mu);
-    DeviceGuard dg(h->device);
+static int host_batch(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
+                      double* pipelinep, double* per_group, int8_t* order, int32_t* invalid) {
     const int km = h->k * h->m;
     // Decoupled pipeline over a span of up to 2^22 layouts held on the
     // device: all H2D chunk copies back to back on one copy stream (the host
@@ -766,6 +760,23 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     CK(cudaStreamSynchronize(h->cs[1]), "sync");
     if (invalid) CK(cudaMemcpy(invalid, h->cinv, sizeof(int), cudaMemcpyDeviceToHost), "D2H invalid");
     return 0;
+}
+
+int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double* total, double* datap,
+                       double* pipelinep, double* per_group, int8_t* order, int32_t* invalid) {
+    if (!h) return fail(-2, "null handle");
+    if (P < 0) return fail(-2, "negative batch");
+    if (invalid) *invalid = 0;
+    if (P == 0) return 0;
+    std::lock_guard<std::mutex> lk(h->mu);
+    DeviceGuard dg(h->device);
+    const int rc = host_batch(h, groups, P, total, datap, pipelinep, per_group, order, invalid);
+    if (rc) {  // nothing of a failed call may still run into the next one's buffers
+        for (cudaStream_t s : {h->cup, h->cs[0], h->cs[1], h->cdown})
+            if (s) cudaStreamSynchronize(s);
+        cudaGetLastError();
+    }
+    return rc;
 }
 
 int hs_bottleneck_batch(const double* w, int m, int64_t B, double* out, int device, void* stream) {
