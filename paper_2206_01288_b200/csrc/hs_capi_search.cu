@@ -352,7 +352,12 @@ static int refine_common(hs_instance* h, int kind, int max_passes, int single, i
     DevBuf<double> dcost;
     DevBuf<int> dev, dch;
     DevBuf<double> hks;
-    if (h->k > 8) CK(hks.alloc((size_t)B * hs::hk_big_size(h->k)), "cudaMalloc");
+    const char* benv = getenv("HS_GA_BATCH");
+    // d_pp 9..16: every partition's snapshots priced in one batch through
+    // the stage + cluster Held-Karp kernels (HS_GA_BATCH=0: in-kernel, one
+    // 4.2 MB Held-Karp slice per partition)
+    const bool batch = !single && h->k > 8 && h->two.rwords && !(benv && benv[0] == '0');
+    if (h->k > 8 && !batch) CK(hks.alloc((size_t)B * hs::hk_big_size(h->k)), "cudaMalloc");
     CK(dg_in.alloc((size_t)B * km), "cudaMalloc");
     CK(dg_out.alloc((size_t)B * km), "cudaMalloc");
     CK(drng.alloc(B), "cudaMalloc");
@@ -383,7 +388,25 @@ static int refine_common(hs_instance* h, int kind, int max_passes, int single, i
     a.hkb = h->hkb;
     a.hk_scratch = hks.p;
     a.hk_size = h->k > 8 ? hs::hk_big_size(h->k) : 0;
+    DevBuf<int16_t> dsnap;
+    DevBuf<double> dscost;
+    DevBuf<int> dscnt, dinv;
+    if (batch) {
+        a.snap_stride = 1 + max_passes;
+        CK(dsnap.alloc((size_t)B * a.snap_stride * km), "cudaMalloc");
+        CK(dscost.alloc((size_t)B * a.snap_stride), "cudaMalloc");
+        CK(dscnt.alloc(B), "cudaMalloc");
+        CK(dinv.alloc(1), "cudaMalloc");
+        a.snap_buf = dsnap.p;
+        a.snap_cnt = dscnt.p;
+    }
     if (hs::launch_refine(a, plan, B, h->rank16 != nullptr, 0)) return fail(-1, "refine launch", cudaGetLastError());
+    if (batch) {
+        if (int rc2 = hs_eval_batch(h, dsnap.p, (int64_t)B * a.snap_stride, dscost.p, nullptr, nullptr, nullptr,
+                                    nullptr, dinv.p, nullptr))
+            return rc2;
+        if (hs::launch_refine_commit(a, dscost.p, B, 0)) return fail(-1, "refine commit launch", cudaGetLastError());
+    }
     CK(cudaDeviceSynchronize(), "refine");
     CK(cudaMemcpy(out, dg_out.p, (size_t)B * km * 2, cudaMemcpyDeviceToHost), "D2H");
     CK(cudaMemcpy(rng, drng.p, sizeof(hs_pcg64) * B, cudaMemcpyDeviceToHost), "D2H");

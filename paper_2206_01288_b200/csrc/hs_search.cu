@@ -149,6 +149,31 @@ __global__ void __launch_bounds__(32) pass_kernel(PassArgs a) {
     }
 }
 
+// _refine's selection (scheduler.py:483-487) over batch-priced snapshots:
+// first strict minimum; one warp per partition
+__global__ void refine_commit_kernel(RefineArgs a, const double* __restrict__ cost, int B) {
+    const int lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (b >= B) return;
+    const int km = a.k * a.m, n = a.snap_cnt[b];
+    const double* c = cost + (size_t)b * a.snap_stride;
+    int bsi = 0;
+    for (int q = 1; q < n; q++)
+        if (c[q] < c[bsi]) bsi = q;
+    const int16_t* src = a.snap_buf + ((size_t)b * a.snap_stride + bsi) * km;
+    for (int t = lane; t < km; t += 32) a.out_groups[(size_t)b * km + t] = src[t];
+    if (lane == 0) {
+        a.out_cost[b] = c[bsi];
+        a.evaluations[b] = n;
+    }
+}
+
+int launch_refine_commit(const RefineArgs& a, const double* snap_cost, int B, cudaStream_t st) {
+    if (B == 0) return 0;
+    refine_commit_kernel<<<(B + 7) / 8, 256, 0, st>>>(a, snap_cost, B);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 size_t pass_smem_bytes(int n, int k, int m) {
     auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
     int cap = m + 1;

@@ -70,7 +70,16 @@ struct RefineArgs {
     double* out_cost;       // [B]
     int* evaluations;       // [B]
     int* changed;           // [B] (single_pass)
+    // batch pricing (d_pp 9..16): the passes' snapshots go to snap_buf
+    // (partition b: slots [b * snap_stride, + snap_cnt[b]), the rest marked
+    // invalid) instead of being priced in-kernel; refine_commit picks
+    int16_t* snap_buf;
+    int* snap_cnt;
+    int snap_stride;
 };
+
+// first-minimum snapshot per partition from the batch-priced snap_cost
+int launch_refine_commit(const RefineArgs& a, const double* snap_cost, int B, cudaStream_t st);
 
 // one pass, no pricing (any d_pp <= 32)
 struct PassArgs {

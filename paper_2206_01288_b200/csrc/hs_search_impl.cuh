@@ -1990,9 +1990,15 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
             ctl[0] = nsnap;
             rng.store(a.rng[b]);
         }
+        if (a.snap_buf && !a.single_pass) {  // snapshots out for batch pricing
+            int16_t* dst = a.snap_buf + (size_t)b * a.snap_stride * km;
+            copy16(dst, snaps, nsnap * km, lane);
+            for (int q = nsnap + lane; q < a.snap_stride; q += kWarp) dst[(size_t)q * km] = -1;
+            if (lane == 0) a.snap_cnt[b] = nsnap;
+        }
     }
     __syncthreads();
-    if (a.single_pass) return;
+    if (a.single_pass || a.snap_buf) return;
     const int nsnap = ctl[0];
     pr.all(snaps, nsnap, km, snapcost, wid, W, lane);
     __syncthreads();

@@ -289,6 +289,38 @@ def test_local_search_d_pp_16_vs_oracle():
             assert [list(x) for x in out.groups] == want.tolist()
 
 
+@pytest.mark.parametrize("kind", ["ours", "kl"])
+def test_batch_priced_local_search_d_pp_16(kind, monkeypatch):
+    """hs_local_search on 12 config-4 partitions: the passes' snapshots of
+    all partitions priced in one batch (stage + cluster Held-Karp) == the
+    in-kernel pricing (HS_GA_BATCH=0) == the oracle's local_search."""
+    from paper_2206_01288_b200 import _native as N
+    g, w = I.instance("config4")
+    rng = np.random.default_rng(8)
+    parts = np.stack([np.array(S.random_partition(rng, g.n, w.d_pp, w.d_dp).groups, dtype=np.int16)
+                      for _ in range(12)])
+    inst = N.instance_for(g, w)
+
+    def run():
+        st = S._states([np.random.default_rng(300 + i) for i in range(len(parts))])
+        out = np.empty_like(parts)
+        tot = np.empty(len(parts))
+        ev = np.empty(len(parts), dtype=np.int32)
+        N.check(N.lib().hs_local_search(inst.handle, S._KIND[kind], 8, len(parts), parts.ctypes.data, st,
+                                        out.ctypes.data, tot.ctypes.data, ev.ctypes.data), "hs_local_search")
+        return out, tot, ev
+
+    batched = run()
+    monkeypatch.setenv("HS_GA_BATCH", "0")
+    in_kernel = run()
+    for x, y in zip(batched, in_kernel):
+        assert np.array_equal(x, y)
+    orc = O.Oracle.of(g, w)
+    for i in range(3):
+        want = orc.local_search(parts[i].astype(np.int32), kind, O.rng_state(np.random.default_rng(300 + i)))
+        assert batched[0][i].tolist() == want.tolist()
+
+
 @pytest.mark.parametrize("kind", ["ours", "kl", "none"])
 def test_warp_island_mode_equals_cta_mode(kind):
     """One warp per island gives the same results as one CTA per island."""
