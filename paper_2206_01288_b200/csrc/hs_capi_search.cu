@@ -27,13 +27,33 @@ hs::SearchShape shape_of(const hs_instance* h, int max_passes) {
 
 const void* rank_of(const hs_instance* h) { return h->rank16 ? (const void*)h->rank16 : (const void*)h->rank; }
 
+// Per-call device scratch from the device's stream-ordered pool (allocated
+// and freed on the legacy stream the calls use; the pool keeps the memory
+// between calls -- a batch of 1,024 config-5 partitions needs 400 MB of mean
+// caches, which cudaMalloc / cudaFree would hand back and re-map every call).
+void keep_pool_memory() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+    done_dev = dev;
+}
+
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
     ~DevBuf() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, 0);
     }
-    cudaError_t alloc(size_t n) { return cudaMalloc(&p, std::max<size_t>(1, n) * sizeof(T)); }
+    cudaError_t alloc(size_t n) {
+        keep_pool_memory();
+        return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, n) * sizeof(T), 0);
+    }
 };
 
 int check_search_shape(const hs_instance* h, int kind, int max_passes) {

@@ -128,6 +128,8 @@ __global__ void __launch_bounds__(32) pass_kernel(PassArgs a) {
     s.home = reinterpret_cast<double*>(take((size_t)n * 8));
     s.valid = reinterpret_cast<int*>(take(16));
     s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+    s.bpv = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.bpp = reinterpret_cast<int16_t*>(take((size_t)n * 2));
     s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
     s.nlocked = reinterpret_cast<int*>(take(4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
@@ -178,8 +180,9 @@ size_t pass_smem_bytes(int n, int k, int m) {
     auto al = [](size_t x) { return (x + 15) & ~(size_t)15; };
     int cap = m + 1;
     return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)k * 4) + al((size_t)n * 8) + al(16) +
-           al((size_t)k * 4) + al((size_t)((n + 31) >> 5) * 4) + al(4) + al((size_t)(k * k + cap) * 2) +
-           al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
+           al((size_t)k * 4) + al((size_t)n * 8) + al((size_t)n * 2) + al((size_t)((n + 31) >> 5) * 4) + al(4) +
+           al((size_t)(k * k + cap) * 2) + al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) +
+           al((size_t)n);
 }
 
 int launch_pass(const PassArgs& a, int B, cudaStream_t st) {
@@ -198,7 +201,7 @@ static size_t ls_bytes(int n, int k, int m) {
     auto al = [](size_t b) { return (b + 15) & ~(size_t)15; };
     return al((size_t)k * cap * 2) + al((size_t)k * 4) + al((size_t)n * k * 8) + al((size_t)n * k * 4) +
            al((size_t)k * 4) + al((size_t)n * 8) + al(16) +
-           al((size_t)k * 4) +
+           al((size_t)k * 4) + al((size_t)n * 8) + al((size_t)n * 2) +
            al((size_t)((n + 31) >> 5) * 4) + al(4) + al((size_t)(k * k + cap) * 2) +
            al((size_t)(4 * cap + 2 * k + 2) * 8) + al((size_t)(3 * k + 8) * 4) + al((size_t)n);
 }

@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(256) ga_spec_kernel(GAArgs a, ScratchLayout wl
     s.home = reinterpret_cast<double*>(take((size_t)n * 8));
     s.valid = reinterpret_cast<int*>(take(16));
     s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+    s.bpv = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.bpp = reinterpret_cast<int16_t*>(take((size_t)n * 2));
     s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
     s.nlocked = reinterpret_cast<int*>(take(4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));

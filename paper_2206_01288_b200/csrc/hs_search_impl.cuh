@@ -75,8 +75,10 @@ struct LS {
     uint32_t* mver;   // n x k: version of the group a mean entry was computed for
     uint32_t* cver;   // k: group content versions (bumped on every change)
     double* home;     // n: cheapest intra-group link of each device
-    int* valid;       // [0]: mean columns valid, [1]: home groups valid, [2]: fast edges valid (bitmasks)
+    int* valid;       // [0]: mean columns valid, [1]: home groups valid, [2]: fast edges valid, [3]: best partners valid (bitmasks)
     int16_t* fe;      // k x 2 cached _fast_edge pairs
+    double* bpv;      // n: each device's cheapest intra-group link (value) ...
+    int16_t* bpp;     // n: ... and its partner (valid[3]: per group, groups of != 8 members)
     uint32_t* locked;  // n-bit set
     int* nlocked;
     int16_t* perm;    // C(k,2)
@@ -218,8 +220,50 @@ __device__ __forceinline__ double mean_at(LS& s, int u, int i) {
 
 static __device__ long long* g_prof = nullptr;
 
+// pair key: (smaller id, larger id) -- members ascend, so the reference's
+// "first minimum in scan order" is the minimum by (value, key)
+__device__ __forceinline__ int pair_key(int x, int y) { return x < y ? x * 1024 + y : y * 1024 + x; }
+
+__device__ __forceinline__ void argmin_vk(double& v, int& key, int& who) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double v2 = __shfl_xor_sync(kFull, v, o);
+        const int k2 = __shfl_xor_sync(kFull, key, o), w2 = __shfl_xor_sync(kFull, who, o);
+        if (v2 < v || (v2 == v && k2 < key)) {
+            v = v2;
+            key = k2;
+            who = w2;
+        }
+    }
+}
+
+// best partner of x in group g (c members), minimum by (W[x][y], key); the
+// warp cooperates, every lane returns it (W is symmetric: scheduler.py:76)
+__device__ inline void best_partner_row(const LS& s, const int16_t* g, int c, int x, int lane, double& bv, int& bp) {
+    const double* wx = s.W + (size_t)x * s.n;
+    double v = kInf;
+    int key = INT_MAX, who = -1;
+    for (int t = lane; t < c; t += kWarp) {
+        const int y = g[t];
+        if (y == x) continue;
+        const double w = wx[y];
+        const int ky = pair_key(x, y);
+        if (w < v || (w == v && ky < key)) {
+            v = w;
+            key = ky;
+            who = y;
+        }
+    }
+    argmin_vk(v, key, who);
+    bv = v;
+    bp = who;
+}
+
 // _fast_edge (:237-249): lexicographically first minimum intra-group pair,
-// lanes over (i, l) pairs, cached per group until the group changes.
+// cached per group until the group changes.  Groups of 8 (the common
+// paper shape): lanes over the 28 position pairs.  Other sizes: the group's
+// minimum over its members' best partners (bpv / bpp, built eight rows at a
+// time when missing, then kept up to date swap by swap in pass_sweep).
 __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
     if ((unsigned)s.valid[2] >> j & 1u) {
         a = s.fe[2 * j];
@@ -229,9 +273,9 @@ __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
     long long f0 = clock64();
     const int16_t* g = s.G + j * s.cap;
     const int c = s.sz[j];
-    double bv = kInf;
-    int code = INT_MAX;
     if (c == 8) {
+        double bv = kInf;
+        int code = INT_MAX;
         if (lane < 28) {  // lane -> (i, l), i < l, lexicographic
             int i = 0, t = lane;
             while (t >= 7 - i) {
@@ -242,33 +286,75 @@ __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
             bv = s.W[(size_t)g[i] * s.n + g[l]];
             code = i * 256 + l;
         }
+        warp_argmin(bv, code);
+        if (code == INT_MAX) code = 1;  // (grp[0], grp[1]) default
+        a = g[code >> 8];
+        b = g[code & 255];
     } else {
-        // eight rows at a time, lanes over the partners l > i (32 per step):
-        // independent loads in flight; minimum by (value, code), so the
-        // lexicographically first pair wins ties whatever the visit order
-        for (int i0 = 0; i0 < c - 1; i0 += 8) {
-            for (int l0 = i0 + 1; l0 < c; l0 += kWarp) {
-                double v[8];
+        if (!((unsigned)s.valid[3] >> j & 1u)) {
+            // every member's best partner: eight rows at a time, lanes over
+            // the partners (independent loads in flight), one argmin per row
+            for (int i0 = 0; i0 < c; i0 += 8) {
+                for (int l0 = 0; l0 < c; l0 += kWarp) {
+                    double v[8];
+                    const int l = l0 + lane;
+                    const int y = l < c ? g[l] : -1;
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int i = i0 + r, l = l0 + r + lane;
-                    v[r] = (i < c - 1 && l > i && l < c) ? s.W[(size_t)g[i] * s.n + g[l]] : kInf;
-                }
+                    for (int r = 0; r < 8; r++) {
+                        const int i = i0 + r;
+                        v[r] = (i < c && y >= 0 && l != i) ? s.W[(size_t)g[i] * s.n + y] : kInf;
+                    }
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int cr = (i0 + r) * 256 + (l0 + r + lane);
-                    if (v[r] < bv || (v[r] == bv && cr < code)) {
-                        bv = v[r];
-                        code = cr;
+                    for (int r = 0; r < 8; r++) {
+                        const int i = i0 + r;
+                        if (i >= c) break;
+                        const int x = g[i];
+                        double bv = v[r];
+                        int key = (y >= 0 && l != i) ? pair_key(x, y) : INT_MAX, who = (y >= 0 && l != i) ? y : -1;
+                        argmin_vk(bv, key, who);
+                        if (l0 > 0) {  // merge with the earlier column chunk
+                            const double ov = s.bpv[x];
+                            const int op = s.bpp[x], ok = op >= 0 ? pair_key(x, op) : INT_MAX;
+                            if (!(bv < ov || (bv == ov && key < ok))) {
+                                bv = ov;
+                                who = op;
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) {
+                            s.bpv[x] = bv;
+                            s.bpp[x] = (int16_t)who;
+                        }
+                        __syncwarp();
                     }
                 }
             }
+            if (lane == 0) s.valid[3] |= (int)(1u << j);
+            __syncwarp();
+        }
+        // the group's fast edge: minimum over its members' best partners
+        double bv = kInf;
+        int key = INT_MAX, who = -1;
+        for (int t = lane; t < c; t += kWarp) {
+            const int x = g[t], y = s.bpp[x];
+            if (y < 0) continue;
+            const double v = s.bpv[x];
+            const int ky = pair_key(x, y);
+            if (v < bv || (v == bv && ky < key)) {
+                bv = v;
+                key = ky;
+                who = x;
+            }
+        }
+        argmin_vk(bv, key, who);
+        if (key == INT_MAX) {
+            a = g[0];  // fewer than two members: (grp[0], grp[1])
+            b = g[1];
+        } else {
+            a = key >> 10;
+            b = key & 1023;
         }
     }
-    warp_argmin(bv, code);
-    if (code == INT_MAX) code = 1;  // (grp[0], grp[1]) default
-    a = g[code >> 8];
-    b = g[code & 255];
     __syncwarp();
     if (lane == 0) {
         s.fe[2 * j] = (int16_t)a;
@@ -278,6 +364,64 @@ __device__ inline void fast_edge(LS& s, int j, int lane, int& a, int& b) {
             g_prof[9] += clock64() - f0;
             g_prof[10] += 1;
         }
+    }
+    __syncwarp();
+}
+
+// group j lost `out` and gained `in` (a _swap); its members' best partners
+// were valid before: the joiner scans its row, everyone else compares the
+// joiner and re-scans only if its best partner was the one who left
+__device__ inline void best_partners_swap(LS& s, int j, int out, int in, int lane) {
+    const int16_t* g = s.G + j * s.cap;
+    const int c = s.sz[j];
+    const double* win = s.W + (size_t)in * s.n;
+    // joiner's row (also each member's link to the joiner: W symmetric)
+    double jv = kInf;
+    int jkey = INT_MAX, jwho = -1;
+    for (int t = lane; t < c; t += kWarp) {
+        const int x = g[t];
+        if (x == in) continue;
+        const double w = win[x];
+        const int kx = pair_key(in, x);
+        if (w < jv || (w == jv && kx < jkey)) {
+            jv = w;
+            jkey = kx;
+            jwho = x;
+        }
+        if (s.bpp[x] != out) {
+            const double ov = s.bpv[x];
+            const int ok = s.bpp[x] >= 0 ? pair_key(x, s.bpp[x]) : INT_MAX;
+            if (w < ov || (w == ov && kx < ok)) {
+                s.bpv[x] = w;
+                s.bpp[x] = (int16_t)in;
+            }
+        }
+    }
+    argmin_vk(jv, jkey, jwho);
+    __syncwarp();
+    // members whose best partner left: a full row each
+    for (int t0 = 0; t0 < c; t0 += kWarp) {
+        const int t = t0 + lane;
+        unsigned redo = __ballot_sync(kFull, t < c && g[t] != in && s.bpp[g[t]] == out);
+        while (redo) {
+            const int u = __ffs(redo) - 1;
+            redo &= redo - 1;
+            const int x = g[t0 + u];
+            double bv;
+            int bp;
+            best_partner_row(s, g, c, x, lane, bv, bp);
+            __syncwarp();
+            if (lane == 0) {
+                s.bpv[x] = bv;
+                s.bpp[x] = (int16_t)bp;
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+        s.bpv[in] = jv;
+        s.bpp[in] = (int16_t)jwho;
+        s.valid[3] |= (int)(1u << j);
     }
     __syncwarp();
 }
@@ -353,6 +497,7 @@ __device__ inline double best_candidate(LS& s, int j, int j2, int lane, int& oa,
 __device__ __forceinline__ void invalidate(LS& s, int j) {
     s.valid[1] &= (int)~(1u << j);
     s.valid[2] &= (int)~(1u << j);
+    s.valid[3] &= (int)~(1u << j);
     s.cver[j]++;
 }
 
@@ -360,6 +505,7 @@ __device__ __forceinline__ void invalidate(LS& s, int j) {
 __device__ __forceinline__ void invalidate_atomic(LS& s, int j) {
     atomicAnd(&s.valid[1], (int)~(1u << j));
     atomicAnd(&s.valid[2], (int)~(1u << j));
+    atomicAnd(&s.valid[3], (int)~(1u << j));
     atomicAdd(&s.cver[j], 1u);
 }
 
@@ -560,11 +706,15 @@ static __device__ __noinline__ bool pass_sweep(LS& s, Pcg64& rng, int lane) {
             }
             if (gain <= 0.0) break;
             g_swap_w(s, a, j, b, j2, lane);  // _swap (:252-257)
+            const unsigned bpv = (unsigned)s.valid[3];
+            __syncwarp();
             if (lane == 0) {
                 invalidate(s, j);
                 invalidate(s, j2);
             }
             __syncwarp();
+            if (bpv >> j & 1u) best_partners_swap(s, j, a, b, lane);
+            if (bpv >> j2 & 1u) best_partners_swap(s, j2, b, a, lane);
             changed = true;
         }
     }
@@ -1242,6 +1392,7 @@ static __device__ bool pass_chains8(LS& s, int lane) {
     if (lane == 0) {
         s.valid[1] = 0;
         s.valid[2] = 0;
+        s.valid[3] = 0;
     }
     __syncwarp();
     return changed;
@@ -1325,6 +1476,7 @@ __device__ __forceinline__ void load_groups(LS& s, const int16_t* p, int lane) {
         s.valid[0] = 0;
         s.valid[1] = 0;
         s.valid[2] = 0;
+        s.valid[3] = 0;
     }
     __syncwarp();
 }
@@ -1584,6 +1736,8 @@ __global__ void __launch_bounds__(256) ga_kernel(GAArgs a, ScratchLayout wl) {
         s.home = reinterpret_cast<double*>(take((size_t)n * 8));
         s.valid = reinterpret_cast<int*>(take(16));
         s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+        s.bpv = reinterpret_cast<double*>(take((size_t)n * 8));
+        s.bpp = reinterpret_cast<int16_t*>(take((size_t)n * 2));
         s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
         s.nlocked = reinterpret_cast<int*>(take(4));
         s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
@@ -1952,6 +2106,8 @@ __global__ void __launch_bounds__(256) refine_kernel(RefineArgs a, ScratchLayout
     s.home = reinterpret_cast<double*>(take((size_t)n * 8));
     s.valid = reinterpret_cast<int*>(take(16));
     s.fe = reinterpret_cast<int16_t*>(take((size_t)k * 4));
+    s.bpv = reinterpret_cast<double*>(take((size_t)n * 8));
+    s.bpp = reinterpret_cast<int16_t*>(take((size_t)n * 2));
     s.locked = reinterpret_cast<uint32_t*>(take((size_t)((n + 31) >> 5) * 4));
     s.nlocked = reinterpret_cast<int*>(take(4));
     s.perm = reinterpret_cast<int16_t*>(take((size_t)(k * k + cap) * 2));
