@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(kClusterThreads, HS_HK_MINB) hk_cluster_kernel
                     default: two_source<15>(Es, own, rw, full, t.dwords, to); break;
                 }
             }
+            HS_JITTER();
             if (p < k) cl_arrive_relaxed();
         }
         {  // layer k: the full set's k entries, slots 0..k-1 of CTA 0

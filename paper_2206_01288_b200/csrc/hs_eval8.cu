@@ -301,6 +301,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
     int64_t chunk = -1, done = 0;  // streamed batch: current chunk, quads finished in it
     auto chunk_of = [&](int64_t q) { return q * kC < a.c0 ? 0 : 1 + (q * kC - a.c0) / a.c; };
     auto report = [&]() {  // this warp is past `chunk`
+        HS_JITTER();
         if (chunk >= 0 && lane == 0) {
             __threadfence();  // the chunk's outputs before its count
             atomicAdd(a.finished + chunk, (uint32_t)done);
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(32 * kE8Warps, 1) eval8_kernel(EvalArgs a) {
                     }
                 }
                 __syncwarp();
+                HS_JITTER();
             }
             done++;
         }
