@@ -157,6 +157,22 @@ def test_chunked_host_path_crosses_chunk_boundary():
     assert np.all(np.isfinite(r["total"]))
 
 
+@pytest.mark.parametrize("case", [1, 2, 3, 4, 5])
+def test_stage_order_and_per_group_at_8x8_vs_oracle(case):
+    """comm_cost's full CostBreakdown at N = 64, 8x8 (per-group values and
+    the stage order) == the oracle's, ties included (cases 1-3 have two
+    distinct link costs)."""
+    g, w = I.instance(f"case{case}")
+    parts = _random_parts(900 + case, 3000, 64, 8, 8)
+    r = hs.comm_cost_batch(g, parts, w, per_group=True, order=True)
+    orc = O.Oracle.of(g, w)
+    for i in range(0, len(parts), 7):
+        tot, dp, pp, pg, order = orc.comm_cost(parts[i])
+        assert r["total"][i] == tot and r["datap"][i] == dp and r["pipelinep"][i] == pp
+        assert np.array_equal(r["per_group"][i], pg)
+        assert r["order"][i].tolist() == order.tolist(), (i, r["order"][i], order)
+
+
 @pytest.mark.parametrize("P", [1, 3, 4097, 36864, 100003])
 def test_streamed_host_path_equals_device_path(P):
     """The host-buffer path at N = 64, 8x8 runs one kernel that consumes its
