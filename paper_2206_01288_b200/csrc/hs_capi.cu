@@ -414,7 +414,7 @@ static int instance_init(hs_instance* h, const double* lat, const double* bw, do
         if (!hs::get_hk_two(h->device, d_pp, &h->two)) {
             h->two_grid = hs::cluster_grid(h->two, h->sm_count);
             h->stage_blocks = h->sm_count * 16;
-            h->two_chunk = 1024;
+            h->two_chunk = getenv("HS_TWO_CHUNK") ? std::max(64, atoi(getenv("HS_TWO_CHUNK"))) : 1024;
         }
     } else {
         hs::EvalArgs a = base_args(h);
