@@ -149,7 +149,7 @@ def test_chunked_host_path_crosses_chunk_boundary():
     g, w = I.instance("case2")
     parts = _random_parts(5, (1 << 18) + 1000, 64, 8, 8)
     r = hs.comm_cost_batch(g, parts, w)
-    # host chunks: a first chunk of 2^13, then 2^16 each (hs_eval_batch_host)
+    # host chunks (hs_eval_batch_host): per-launch 2^13 then 2^16, streamed 2^12 then 2^15
     b0, b1 = 1 << 13, (1 << 13) + (1 << 16)
     sel = np.r_[0:50, b0 - 25:b0 + 25, b1 - 25:b1 + 25, (1 << 18) - 25:(1 << 18) + 25, len(parts) - 50:len(parts)]
     t, _, _ = O.Oracle.of(g, w).comm_cost_batch(parts[sel], threads=O.cpu_count())
@@ -185,6 +185,24 @@ def test_streamed_host_path_equals_device_path(P):
     dev = hs.comm_cost_batch(g, torch.from_numpy(parts).cuda(), w, per_group=True)
     for key in host:
         assert np.array_equal(host[key], dev[key].cpu().numpy()), key
+
+
+@pytest.mark.parametrize("P", [5, 70001])
+def test_per_chunk_launch_host_path_equals_streamed(P, monkeypatch):
+    """HS_HOST_STREAMED=0 (one eval8 launch per host chunk on alternating
+    compute streams, read per call) prices exactly like the default streamed
+    kernel, per-group outputs and a malformed row included."""
+    g, w = I.instance("case5")
+    parts = _random_parts(70 + P % 5, P, 64, 8, 8)
+    a = hs.comm_cost_batch(g, parts, w, per_group=True)
+    monkeypatch.setenv("HS_HOST_STREAMED", "0")
+    b = hs.comm_cost_batch(g, parts, w, per_group=True)
+    for key in a:
+        assert np.array_equal(a[key], b[key]), key
+    bad = parts.copy()
+    bad[P // 2, 0, 0] = bad[P // 2, 1, 0]
+    with pytest.raises(hs.CostModelError, match=f"1 of {P}"):
+        hs.comm_cost_batch(g, bad, w)
 
 
 def test_host_path_spans_more_than_its_device_buffers():
