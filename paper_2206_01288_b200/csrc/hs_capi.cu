@@ -774,6 +774,11 @@ int hs_eval_batch_host(hs_instance* h, const int16_t* groups, int64_t P, double*
     if (rc) {  // nothing of a failed call may still run into the next one's buffers
         for (cudaStream_t s : {h->cup, h->cs[0], h->cs[1], h->cdown})
             if (s) cudaStreamSynchronize(s);
+        // the streamed kernel counts every chunk it finished, also those
+        // whose D2H wait was never enqueued: restart from the device counts
+        if (h->finished && h->nslots &&
+            cudaMemcpy(h->fin_target.data(), h->finished, (size_t)h->nslots * 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+            h->nslots = 0;  // unknown counts: the next streamed call reallocates and zeroes them
         cudaGetLastError();
     }
     return rc;
