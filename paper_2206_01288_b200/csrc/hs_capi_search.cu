@@ -1,7 +1,9 @@
 // hs_capi_search.cu -- C-ABI of the search kernels (include/hetsched_b200.h).
 #include <algorithm>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "hs_big.h"
@@ -27,21 +29,35 @@ hs::SearchShape shape_of(const hs_instance* h, int max_passes) {
 
 const void* rank_of(const hs_instance* h) { return h->rank16 ? (const void*)h->rank16 : (const void*)h->rank; }
 
-// Per-call device scratch from the device's stream-ordered pool (allocated
-// and freed on the legacy stream the calls use; the pool keeps the memory
-// between calls -- a batch of 1,024 config-5 partitions needs 400 MB of mean
-// caches, which cudaMalloc / cudaFree would hand back and re-map every call).
-void keep_pool_memory() {
-    static thread_local int done_dev = -1;
+// Per-call device scratch from a stream-ordered pool of this library's own
+// per device (allocated and freed on the legacy stream the calls use; the
+// pool keeps the memory between calls -- a batch of 1,024 config-5
+// partitions needs 400 MB of mean caches, which cudaMalloc / cudaFree would
+// hand back and re-map every call).  The device's default pool, which other
+// code in the process may use, is left alone.
+constexpr int kMaxPoolDevices = 64;
+
+cudaMemPool_t scratch_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[kMaxPoolDevices] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxPoolDevices) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
         uint64_t keep = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        pools[dev] = pool;
     }
-    cudaGetLastError();
-    done_dev = dev;
+    return pools[dev];
 }
 
 template <typename T>
@@ -51,8 +67,9 @@ struct DevBuf {
         if (p) cudaFreeAsync(p, 0);
     }
     cudaError_t alloc(size_t n) {
-        keep_pool_memory();
-        return cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, n) * sizeof(T), 0);
+        cudaMemPool_t pool = scratch_pool();
+        if (!pool) return cudaErrorMemoryAllocation;
+        return cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p), std::max<size_t>(1, n) * sizeof(T), pool, 0);
     }
 };
 
